@@ -1,0 +1,280 @@
+"""CPU oracle wrapper -- TEST INFRASTRUCTURE, not the product.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+``--impl reference``) may import this module, as the checker or as the reported
+CPU baseline. The product package ``paper_2112_10517_b200`` never imports it.
+
+It wraps ``liboracle.so`` (fdg_oracle.c, built by ``oracle/Makefile``), a
+plain-C restatement of the reference's scalar flux-differencing path that is
+pinned BITWISE to the reference's own outputs (tests/golden/*.npz, written by
+tests/golden/make_golden.py from /root/reference/pkg/src/fluxdg):
+
+* ``volume(u, setup, flux, precompute)`` == ``volume_fluxdiff`` over all
+  elements (reference discretization.py:267-323)
+* ``surface(u, setup, flux, out)``       == ``surface_terms`` LGL branch
+  (discretization.py:681-760)
+* ``rhs(u, setup, vflux, sflux, precompute)`` == ``rhs(kernel="reference")``
+  (discretization.py:896-949), including the admissibility gate message
+  (discretization.py:660-672)
+* ``rk54_step`` == ``rk_step`` with the Carpenter-Kennedy RK54 tableau
+  (timeint.py:101-163), same numpy operation sequence
+* ``ssprk43_step`` -- the Shu-Osher SSPRK(4,3) step BASELINE cfg 4 asks for;
+  NOT in the reference (parity unpinned, checked by order conditions).
+
+``setup`` is duck-typed: anything with ``d``, ``op.weights``,
+``dsplit.matrix``, ``metrics.{ja,jac,cartesian}``, ``plus_neighbor`` and
+``gas.{gamma,inv_gamma_minus_one}`` -- the reference's SpatialSetup and the
+product's SpatialSetup both qualify, and so do plain namespaces.
+"""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+
+FLUX_IDS = {
+    "central": 0,
+    "shima": 1,
+    "ranocha": 2,
+    "kennedy_gruber": 3,
+    "chandrashekar": 4,
+    "llf": 5,
+    "hll": 6,
+}
+PRE_IDS = {"none": 0, "primitives": 1, "primitives_and_logs": 2}
+
+
+class OrMesh(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int),
+        ("p1", ctypes.c_int),
+        ("n_elem", ctypes.c_int64),
+        ("dsplit", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("gamma", ctypes.c_double),
+        ("igm1", ctypes.c_double),
+        ("cartesian", ctypes.c_int),
+        ("areas", ctypes.c_void_p),
+        ("jac_const", ctypes.c_double),
+        ("ja", ctypes.c_void_p),
+        ("jac", ctypes.c_void_p),
+        ("plus", ctypes.c_void_p),
+        ("minus", ctypes.c_void_p),
+        ("ghost_u", ctypes.c_void_p),
+        ("ghost_nrm", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def build(force=False):
+    """Compile liboracle.so in place (gcc, strict IEEE flags, see Makefile)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER(OrMesh)
+        vp = ctypes.c_void_p
+        L.or_volume.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.or_surface.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int]
+        L.or_rhs.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.or_rhs.restype = ctypes.c_int64
+        L.or_gate.argtypes = [P, vp, vp, vp]
+        L.or_gate.restype = ctypes.c_int64
+        L.or_two_point.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+            vp, vp, vp, ctypes.c_int, vp,
+        ]
+        L.or_logmean.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.or_logmean.restype = ctypes.c_double
+        L.or_inv_logmean.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.or_inv_logmean.restype = ctypes.c_double
+        L.or_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class MeshArrays:
+    """Contiguous host arrays describing one (possibly partitioned) mesh."""
+
+    def __init__(self, d, p1, n_elem, dsplit, weights, gamma, igm1, cartesian, areas,
+                 jac_const, ja, jac, plus, minus, ghost_u=None, ghost_nrm=None):
+        c = np.ascontiguousarray
+        self.keep = dict(
+            dsplit=c(dsplit, dtype=np.float64),
+            weights=c(weights, dtype=np.float64),
+            areas=c(areas, dtype=np.float64) if areas is not None else None,
+            ja=c(ja, dtype=np.float64) if ja is not None else None,
+            jac=c(jac, dtype=np.float64) if jac is not None else None,
+            plus=c(plus, dtype=np.int64),
+            minus=c(minus, dtype=np.int64),
+            ghost_u=c(ghost_u, dtype=np.float64) if ghost_u is not None else None,
+            ghost_nrm=c(ghost_nrm, dtype=np.float64) if ghost_nrm is not None else None,
+        )
+        k = self.keep
+        self.d, self.p1, self.n_elem = d, p1, n_elem
+        self.struct = OrMesh(
+            d, p1, n_elem, _ptr(k["dsplit"]), _ptr(k["weights"]), gamma, igm1, int(cartesian),
+            _ptr(k["areas"]), jac_const, _ptr(k["ja"]), _ptr(k["jac"]), _ptr(k["plus"]),
+            _ptr(k["minus"]), _ptr(k["ghost_u"]), _ptr(k["ghost_nrm"]),
+        )
+
+
+def mesh_from_setup(setup, lo=0, hi=None):
+    """MeshArrays for elements [lo, hi) of a full periodic setup (no ghosts)."""
+    d = setup.d
+    weights = np.asarray(setup.op.weights)
+    p1 = weights.shape[0]
+    metrics = setup.metrics
+    n_elem = metrics.jac.shape[0] if hasattr(metrics, "jac") and metrics.jac is not None else None
+    plus = np.stack([np.asarray(setup.plus_neighbor[n]) for n in range(d)])
+    n_elem = plus.shape[1]
+    minus = np.empty_like(plus)
+    for n in range(d):
+        minus[n, plus[n]] = np.arange(n_elem)
+    cart = bool(metrics.cartesian)
+    ja = None if cart else np.asarray(metrics.ja)
+    jac = np.asarray(metrics.jac) if getattr(metrics, "jac", None) is not None else None
+    if cart:
+        areas = np.diag(np.asarray(metrics.ja[0, 0])).copy()
+        jac_const = float(metrics.jac[0, 0])
+        jac = None
+    else:
+        areas = None
+        jac_const = 0.0
+    return MeshArrays(
+        d, p1, n_elem, np.asarray(setup.dsplit.matrix), weights, setup.gas.gamma,
+        setup.gas.inv_gamma_minus_one, cart, areas, jac_const, ja, jac, plus, minus,
+    )
+
+
+def _mesh(m):
+    return m if isinstance(m, MeshArrays) else mesh_from_setup(m)
+
+
+def volume(u, setup, flux="ranocha", precompute="none", nthreads=0):
+    m = _mesh(setup)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty_like(u)
+    lib().or_volume(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], PRE_IDS[precompute], nthreads)
+    return out
+
+
+def surface(u, setup, flux="llf", out=None, nthreads=0):
+    m = _mesh(setup)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if out is None:
+        out = np.zeros_like(u)
+    assert out.flags.c_contiguous and out.dtype == np.float64
+    lib().or_surface(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], nthreads)
+    return out
+
+
+class OracleAdmissibilityError(RuntimeError):
+    pass
+
+
+def gate(u, setup):
+    """(element, node, rho, p) of the first inadmissible node, or None."""
+    m = _mesh(setup)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    rho = np.zeros(1)
+    p = np.zeros(1)
+    g = lib().or_gate(ctypes.byref(m.struct), _ptr(u), _ptr(rho), _ptr(p))
+    if g < 0:
+        return None
+    nn = u.shape[1]
+    return int(g // nn), int(g % nn), float(rho[0]), float(p[0])
+
+
+def rhs(u, setup, volume_flux="ranocha", surface_flux="ranocha", precompute="none", nthreads=0):
+    m = _mesh(setup)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    bad = gate(u, m)
+    if bad is not None:
+        e, i, rho, p = bad
+        raise OracleAdmissibilityError(
+            "inadmissible state at element %d, node %d: rho=%r, p=%r" % (e, i, rho, p)
+        )
+    du = np.empty_like(u)
+    lib().or_rhs(
+        ctypes.byref(m.struct), _ptr(u), _ptr(du), FLUX_IDS[volume_flux], FLUX_IDS[surface_flux],
+        PRE_IDS[precompute], nthreads,
+    )
+    return du
+
+
+def two_point(ul, ur, normal, flux, gamma=1.4, cart_axis=-1, precompute="none"):
+    ul = np.ascontiguousarray(ul, dtype=np.float64)
+    ur = np.ascontiguousarray(ur, dtype=np.float64)
+    nrm = np.zeros(3)
+    nrm[: len(normal)] = normal
+    f = np.zeros(5)
+    d = ul.shape[0] - 2
+    lib().or_two_point(d, FLUX_IDS[flux], PRE_IDS[precompute], gamma, 1.0 / (gamma - 1.0),
+                       _ptr(ul), _ptr(ur), _ptr(nrm), cart_axis, _ptr(f))
+    return f[: d + 2]
+
+
+def logmean(a, b):
+    return lib().or_logmean(a, b)
+
+
+def inv_logmean(a, b):
+    return lib().or_inv_logmean(a, b)
+
+
+def max_threads():
+    return lib().or_max_threads()
+
+
+# --- time stepping (numpy, same operation sequence as timeint.py:149-163) ---
+
+RK54_A = (
+    0.0,
+    -567301805773 / 1357537059087,
+    -2404267990393 / 2016746695238,
+    -3550918686646 / 2091501179385,
+    -1275806237668 / 842570457699,
+)
+RK54_B = (
+    1432997174477 / 9575080441755,
+    5161836677717 / 13612068292357,
+    1720146321549 / 2090206949498,
+    3134564353537 / 4481467310338,
+    2277821191437 / 14882151754819,
+)
+
+
+def rk54_step(u, dt, rhs_fn):
+    du = np.zeros_like(u)
+    v = np.array(u, copy=True)
+    for i in range(5):
+        k = rhs_fn(v)
+        du = RK54_A[i] * du + dt * k
+        v = v + RK54_B[i] * du
+    return v
+
+
+def ssprk43_step(u, dt, rhs_fn):
+    """Four-stage third-order SSP RK in Shu-Osher form (NOT in the reference)."""
+    u1 = u + 0.5 * dt * rhs_fn(u)
+    u2 = u1 + 0.5 * dt * rhs_fn(u1)
+    u3 = (2.0 / 3.0) * u + (1.0 / 3.0) * u2 + (1.0 / 6.0) * dt * rhs_fn(u2)
+    return u3 + 0.5 * dt * rhs_fn(u3)

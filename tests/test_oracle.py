@@ -1,0 +1,132 @@
+"""Pin the CPU oracle (oracle/fdg_oracle.c) to the reference's own outputs.
+
+Every comparison against the scalar path is BITWISE (np.array_equal): the
+oracle restates volume_fluxdiff / surface_terms / rhs(kernel="reference")
+operation by operation (reference discretization.py:267-323, 681-760,
+896-949). The batched-path fixtures (batched.py:450-544) are compared at the
+reference's own equivalence tolerance (tests/test_batched.py: 1e-13 abs).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests import golden_io as G
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_volume_bitwise(name):
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    checked = 0
+    for key in c:
+        if not key.startswith("vol_"):
+            continue
+        _, state, flux, pre = key.split("_", 3)
+        got = oracle.volume(c["u_" + state], setup, flux, pre)
+        assert np.array_equal(got, c[key]), key
+        checked += 1
+    assert checked >= 2
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_volume_vs_batched_path(name):
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("volb_"):
+            continue
+        _, state, flux = key.split("_", 2)
+        pre = "none"
+        if flux == "ranocha_logs":
+            flux, pre = "ranocha", "primitives_and_logs"
+        got = oracle.volume(c["u_" + state], setup, flux, pre)
+        scale = max(1.0, np.abs(c[key]).max())
+        assert np.abs(got - c[key]).max() <= 1e-13 * scale, key
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_surface_bitwise(name):
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("surf_"):
+            continue
+        _, state, flux = key.split("_", 2)
+        got = oracle.surface(c["u_" + state], setup, flux)
+        assert np.array_equal(got, c[key]), key
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_rhs_bitwise(name):
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    n = 0
+    for key in c:
+        if not key.startswith("rhs_"):
+            continue
+        parts = key.split("_")
+        state, vf, sf = parts[1], parts[2], parts[3]
+        pre = "primitives_and_logs" if key.endswith("_logs") else "none"
+        got = oracle.rhs(c["u_" + state], setup, vf, sf, pre)
+        assert np.array_equal(got, c[key]), key
+        n += 1
+    assert n >= 1
+
+
+@pytest.mark.parametrize("name", ["c2d_cart_p3", "c3d_curv_p2", "c3d_curv_p4"])
+def test_rk54_bitwise(name):
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    dt = float(c["rk54_dt"])
+    for state in G.states(name):
+        got = oracle.rk54_step(c["u_" + state], dt, lambda v: oracle.rhs(v, setup, "ranocha", "llf"))
+        assert np.array_equal(got, c["rk54_" + state])
+
+
+def test_cfg1_bitwise():
+    c = G.config(1)
+    from types import SimpleNamespace
+
+    # cfg1 = 2D 16x16 Cartesian on [-1,1]^2, N=3 (BASELINE.json configs[0])
+    ops = G.operators()
+    n_elem = 256
+    idx = np.arange(n_elem).reshape(16, 16)
+    plus = tuple(np.roll(idx, -1, axis=n).ravel() for n in range(2))
+    jac_val = (0.5 * 2.0 / 16) ** 2
+    area = jac_val / (0.5 * 2.0 / 16)
+    ja = np.zeros((n_elem, 16, 2, 2))
+    ja[:, :, 0, 0] = area
+    ja[:, :, 1, 1] = area
+    setup = SimpleNamespace(
+        d=2,
+        op=SimpleNamespace(weights=ops["weights_3"]),
+        dsplit=SimpleNamespace(matrix=ops["dsplit_3"]),
+        metrics=SimpleNamespace(ja=ja, jac=np.full((n_elem, 16), jac_val), cartesian=True),
+        plus_neighbor=plus,
+        gas=SimpleNamespace(gamma=1.4, inv_gamma_minus_one=1.0 / (1.4 - 1.0)),
+    )
+    assert np.array_equal(oracle.volume(c["u"], setup, "ranocha"), c["vol"])
+    assert np.array_equal(oracle.surface(c["u"], setup, "llf"), c["surf"])
+    assert np.array_equal(oracle.rhs(c["u"], setup, "ranocha", "llf"), c["du"])
+    assert np.array_equal(
+        oracle.rhs(c["u"], setup, "ranocha", "llf", "primitives_and_logs"), c["du_logs"]
+    )
+
+
+def test_gate_names_first_bad_node():
+    setup = G.golden_setup("c2d_cart_p3")
+    u = G.case("c2d_cart_p3")["u_rand"].copy()
+    u[1, 2, -1] = 0.01
+    u[4, 0, 0] = -1.0
+    with pytest.raises(oracle.OracleAdmissibilityError, match="element 1, node 2"):
+        oracle.rhs(u, setup)
+
+
+def test_logmean_known_values():
+    # equal arguments hit the series branch exactly: L(a, a) = a
+    for a in (0.5, 1.0, 3.7, 1e-3, 1e5):
+        assert oracle.logmean(a, a) == a
+        assert oracle.inv_logmean(a, a) == 1.0 / a
+    # well separated: (b - a)/log(b/a)
+    assert oracle.logmean(1.0, np.e) == pytest.approx(np.e - 1.0, rel=1e-15)
