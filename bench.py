@@ -1,0 +1,361 @@
+"""Benchmark of the flux-differencing volume integral (BASELINE.json metric:
+volume-integral DOF updates/s = 1/PID, fp64).
+
+Workload (BASELINE.json configs[1]): 3D compressible Euler, N=3 (4^3 LGL nodes),
+16^3 periodic Cartesian hexes on [-1,1]^3, Ranocha EC flux, density-wave state
+(rho = 1 + 0.98 sin(pi(x+y+z)), v = (0.1,0.2,0.3), p = 20); one step = one
+volume-integral pass over the mesh (262,144 nodes). The FAST kernels with
+per-node log tables (precompute="primitives_and_logs", the paper's
+technique). The input (10.5 MB) fits in L2, so L2 is flushed (256 MB write)
+between timed launches and each launch is timed on its own with CUDA events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun): the volume integral has no exchange step; every rank
+owns one cfg2-sized slab (weak scaling), value = all nodes / max-rank time.
+--impl reference times the CPU oracle (C restatement of the reference's
+scalar path, bitwise equal to it; all host threads) on the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "volume-integral DOF updates/s (1/PID), fp64"
+UNIT = "DOF/s"
+BYTES_PER_NODE = 80.0  # u read once + VOL written once, 5 doubles each
+FLOP_PER_NODE = 428.5  # Ranocha Cartesian 3D N=3, prim+logs, log branch
+CONFIG_NAME = "cfg2: 3D Euler N=3, 16^3 Cartesian hexes, Ranocha EC, volume integral"
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = (
+        "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+        "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    )
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.QUERY, "--format=csv,noheader,nounits",
+                 "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for name, val in zip(names, r[5:9]):
+                    if val.lower() == "active":
+                        reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def cpu_baseline(setup, u, steps=3):
+    """The oracle (reference arithmetic, bitwise) on the host cores."""
+    from oracle import oracle
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    mesh = oracle.mesh_from_setup(setup)
+    oracle.volume(u, mesh, "ranocha", "primitives_and_logs", nthreads=threads)  # warm-up
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.volume(u, mesh, "ranocha", "primitives_and_logs", nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    nodes = u.shape[0] * u.shape[1]
+    return {
+        "value": nodes / statistics.mean(times),
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": "full cfg2 mesh (4096 elements, 262144 nodes), oracle/fdg_oracle.c volume_fluxdiff order, "
+                  "precompute=primitives_and_logs, %d timed passes after 1 warm-up, mean" % steps,
+        "cpu_model": _cpu_model(),
+    }
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the same workload (rank 0 only)."""
+    if rank != 0:
+        return 0
+    from paper_2112_10517_b200 import workloads
+
+    setup, u, _ = workloads.build(2)
+    from oracle import oracle
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    mesh = oracle.mesh_from_setup(setup)
+    for _ in range(args.warmup):
+        oracle.volume(u, mesh, "ranocha", "primitives_and_logs", nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.volume(u, mesh, "ranocha", "primitives_and_logs", nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    nodes = u.shape[0] * u.shape[1]
+    ms = 1e3 * statistics.mean(times)
+    value = nodes / (ms * 1e-3)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAME, "nodes": nodes, "elements": u.shape[0]},
+        "cpu_baseline": {
+            "value": value,
+            "unit": UNIT,
+            "cores": threads,
+            "kind": "port",
+            "sample": "each step: full cfg2 volume integral (262144 nodes) through oracle/fdg_oracle.c "
+                      "(C restatement of the reference's scalar path, bitwise equal to it), pthreads",
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _traffic_from_profile():
+    """dram bytes per launch of the volume kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "vol_cfg2_ncu_summary.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2112_10517_b200 import _native as N
+    from paper_2112_10517_b200 import workloads
+    from paper_2112_10517_b200.device import device_mesh_for
+    from paper_2112_10517_b200.discretization import mesh_fluxdiff_volume
+
+    setup, u_host, config = workloads.build(2, kernel="batched")
+    nodes = u_host.shape[0] * u_host.shape[1]
+    dm = device_mesh_for(setup)
+    scheme = config.scheme()
+    stream = torch.cuda.current_stream()
+    u = torch.as_tensor(u_host, device="cuda")
+    vol = dm.empty()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    for _ in range(args.warmup):
+        dm.volume(u, scheme, out=vol)
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = N.launch_count()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict u/VOL from L2 between timed launches
+            starts[i].record(stream)
+            dm.volume(u, scheme, out=vol)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    if dist is not None:
+        dist.barrier()
+    per_launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = statistics.mean(per_launch_ms)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * nodes / (ms * 1e-3)
+
+    # ---- end to end through the public API with pinned host buffers
+    u_pin = torch.empty(u_host.shape, dtype=torch.float64, pin_memory=True)
+    u_pin.copy_(torch.from_numpy(u_host))
+    out_pin = torch.empty(u_host.shape, dtype=torch.float64, pin_memory=True)
+    for _ in range(2):
+        mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
+    e2e_ms = []
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = statistics.mean(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    hbm, peak_src = _peaks()
+    achieved = BYTES_PER_NODE * nodes / (ms * 1e-3) / 1e9
+    fp64_peak = N.fp64_peak_tflops()
+    traffic = _traffic_from_profile()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": CONFIG_NAME,
+            "elements_per_gpu": u_host.shape[0],
+            "nodes_per_gpu": nodes,
+            "kernel": "batched (FAST), precompute=primitives_and_logs",
+            "l2": "flushed (256 MB write) between timed launches; each launch timed alone",
+            "parallelism": "replicas per GPU (element-local, no exchange)" if world > 1 else "single GPU",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": hbm,
+            "unit": "GB/s",
+            "frac": achieved / hbm,
+            "traffic": traffic,
+            "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
+            "algorithmic_bytes_per_node": BYTES_PER_NODE,
+        },
+        "fp64": {
+            "achieved_tflops": FLOP_PER_NODE * nodes / (ms * 1e-3) / 1e12,
+            "peak_tflops_probe": fp64_peak,
+            "frac": FLOP_PER_NODE * nodes / (ms * 1e-3) / 1e12 / fp64_peak if fp64_peak else None,
+            "algorithmic_flop_per_node": FLOP_PER_NODE,
+        },
+        "e2e": {
+            "value": world * nodes / (e2e * 1e-3),
+            "unit": UNIT,
+            "ms_per_step": e2e,
+            "h2d_bytes_per_step": int(u_host.nbytes),
+            "d2h_bytes_per_step": int(u_host.nbytes),
+            "path": "paper_2112_10517_b200.mesh_fluxdiff_volume(pinned CPU tensor) -> libfdg.so fdg_volume",
+        },
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "per_launch_ms": {"min": min(per_launch_ms), "max": max(per_launch_ms)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(setup, u_host)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/* fdg.h -- C ABI of libfdg.so, the B200 (sm_100a) flux-differencing DGSEM
+ * volume integral / RHS for the compressible Euler equations.
+ *
+ * Drop-in boundary for the reference artifact `fluxdg` (arXiv 2112.10517,
+ * /root/reference/pkg/src/fluxdg).  The reference has no FFI; its plugin seam
+ * is the kernel string of RhsConfig (discretization.py:73, 932-936) and the
+ * module-level functions below.  Each entry point replaces one of them:
+ *
+ *   fdg_volume    <- batched.mesh_fluxdiff_volume(u, setup, config)      batched.py:450-511
+ *                    (and discretization.volume_fluxdiff per element,     discretization.py:267-323)
+ *   fdg_surface   <- batched.mesh_surface(u, setup, surface_flux, out)   batched.py:514-544
+ *                    / discretization.surface_terms(..., out=out)         discretization.py:681-788
+ *   fdg_rhs       <- discretization.rhs(u, setup, config)                discretization.py:896-949
+ *   fdg_rk_stage  <- one stage of timeint.rk_step                        timeint.py:149-163
+ *                    (and of SSPRK43, which the reference does not ship)
+ *   fdg_gate      <- discretization._admissibility_gate                  discretization.py:660-672
+ *   fdg_mesh_create <- the device image of build_setup's SpatialSetup    discretization.py:609-657
+ *
+ * Conventions: all state pointers are DEVICE pointers owned by the caller
+ * (torch allocations in the Python host layer); the library allocates only a
+ * 16-byte status record per mesh handle, at creation.  Calls are
+ * stream-ordered and asynchronous; only fdg_read_status synchronizes.
+ * Layout: the reference's own AoS layout, u[e][i][v] = (n_elem, (p+1)^d, d+2),
+ * node index C-ordered over the reference coordinates, variables
+ * (rho, rho v_1..rho v_d, rho E).
+ * Return codes map 1:1 to the reference's exceptions (errors.py):
+ *   FDG_ERR_CONFIG -> ConfigurationError, FDG_ERR_UNSUPPORTED ->
+ *   UnsupportedOperatorError; an inadmissible state is reported through the
+ *   status record (AdmissibilityError on the host, same message format).
+ */
+#ifndef FDG_H
+#define FDG_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDG_ABI_VERSION 1
+
+enum fdg_rc { FDG_OK = 0, FDG_ERR_CONFIG = 1, FDG_ERR_UNSUPPORTED = 2, FDG_ERR_CUDA = 3, FDG_ERR_ARG = 4 };
+
+/* two-point flux kinds (fluxes.py:30-31 plus the BASELINE additions) */
+enum fdg_flux {
+    FDG_FLUX_CENTRAL = 0,
+    FDG_FLUX_SHIMA = 1,
+    FDG_FLUX_RANOCHA = 2,
+    FDG_FLUX_KENNEDY_GRUBER = 3, /* not in the reference (parity unpinned) */
+    FDG_FLUX_CHANDRASHEKAR = 4,  /* not in the reference (parity unpinned) */
+    FDG_FLUX_LLF = 5,            /* surface only (Rusanov) */
+    FDG_FLUX_HLL = 6             /* surface only */
+};
+/* RhsConfig.precompute (discretization.py:72) */
+enum fdg_precompute { FDG_PRE_NONE = 0, FDG_PRE_PRIMITIVES = 1, FDG_PRE_PRIMITIVES_AND_LOGS = 2 };
+/* RhsConfig.kernel: "reference" -> FAITHFUL (scalar path's arithmetic, correctly
+ * rounded log), "batched" -> FAST (FMA, shared reciprocals) */
+enum fdg_mode { FDG_MODE_FAITHFUL = 0, FDG_MODE_FAST = 1 };
+
+typedef struct fdg_mesh fdg_mesh_t;
+
+typedef struct fdg_mesh_desc {
+    int32_t d;             /* 2 or 3 */
+    int32_t degree;        /* p, 1..7 */
+    int64_t n_elem;        /* elements held by this rank */
+    int64_t elem_base;     /* global index of local element 0 (error messages) */
+    double gamma;          /* GasParams.gamma */
+    double inv_gamma_minus_one; /* GasParams.inv_gamma_minus_one */
+    const double *dsplit;  /* HOST (p+1)^2, build_dsplit(op).matrix, row-major */
+    const double *weights; /* HOST (p+1), op.weights */
+    int32_t cartesian;     /* metrics.cartesian: axis fluxes scaled by areas */
+    double areas[3];       /* Cartesian Ja^n_n (diag of metrics.ja[0,0]) */
+    double jac_const;      /* Cartesian J */
+    const double *ja;      /* DEVICE (n_elem, nn, d, d), curved only */
+    const double *jac;     /* DEVICE (n_elem, nn), curved only */
+    const int32_t *plus;   /* DEVICE (d, n_elem): +n neighbour, <0 -> ghost slot -(g+1) */
+    const int32_t *minus;  /* DEVICE (d, n_elem): -n neighbour, <0 -> ghost slot */
+    const double *ghost_nrm; /* DEVICE (n_ghost, fn, d) face normals of remote minus
+                                neighbours (curved partitions), or NULL */
+} fdg_mesh_desc_t;
+
+typedef struct fdg_scheme {
+    int32_t volume_flux;  /* enum fdg_flux, symmetric kinds only */
+    int32_t surface_flux; /* enum fdg_flux */
+    int32_t precompute;   /* enum fdg_precompute */
+    int32_t mode;         /* enum fdg_mode */
+} fdg_scheme_t;
+
+typedef struct fdg_stage {
+    int32_t kind;     /* 0: low-storage 2N  reg = a reg + dt k; v_out = v_in + b reg
+                         1: Shu-Osher      v_out = (A u0 + B v_in) + Cdt k (A == 0: v_in + Cdt k) */
+    uint32_t index;   /* stage number reported on a non-finite result */
+    double a, b, cdt, dt;
+} fdg_stage_t;
+
+typedef struct fdg_status {
+    int64_t first_bad;  /* flat (element * nn + node) of the first inadmissible node, or -1 */
+    int32_t bad_stage;  /* first RK stage with a non-finite result, or -1 */
+    int32_t pad;
+} fdg_status_t;
+
+int fdg_abi_version(void);
+const char *fdg_last_error(void);
+int fdg_supported(int32_t d, int32_t degree);
+unsigned long long fdg_launch_count(void);
+
+int fdg_mesh_create(const fdg_mesh_desc_t *desc, fdg_mesh_t **out);
+void fdg_mesh_destroy(fdg_mesh_t *mesh);
+
+/* VOL = (1/J) sum_n sum_k Dsplit f*_n(u_i, u_k)   (not negated) */
+int fdg_volume(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, double *vol, void *stream);
+/* out += SURF  (LGL interface terms, lifted and /J) */
+int fdg_surface(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, const double *ghost_u,
+                double *out, void *stream);
+/* du = -(VOL + SURF) */
+int fdg_rhs(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, const double *ghost_u, double *du,
+            void *stream);
+/* one Runge-Kutta stage fused with the RHS: v_out must not alias v_in */
+int fdg_rk_stage(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const fdg_stage_t *stage, const double *v_in,
+                 const double *ghost_u, double *v_out, double *reg, const double *u0, void *stream);
+/* admissibility of every node (rho > 0, p > 0, finite) into the status record */
+int fdg_gate(fdg_mesh_t *mesh, const double *u, void *stream);
+int fdg_reset_status(fdg_mesh_t *mesh, void *stream);
+/* synchronizes `stream`, copies the status record out */
+int fdg_read_status(fdg_mesh_t *mesh, fdg_status_t *out, void *stream);
+
+/* halo helper: out[i][m][v] = u[elems[i]][line node m of direction dir at end `side`][v] */
+int fdg_pack_faces(const double *u, const int32_t *elems, int32_t n, int32_t d, int32_t degree, int32_t dir,
+                   int32_t side, double *out, void *stream);
+
+/* sustained FP64 FMA throughput of this device (TFLOP/s, 2 flop per DFMA) */
+int fdg_fp64_probe(double *tflops, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -48,6 +48,19 @@
 
 #define SERIES_EPSILON 1.0e-4 /* means.py:16 */
 
+/* OR_LOG: glibc log (the reference's math.log) by default; with
+ * -DFDG_ORACLE_LOGCR the correctly rounded log_cr that the GPU FAITHFUL mode
+ * uses (same source, paper_2112_10517_b200/csrc/fdg_logcr.h, itself checked
+ * against mpmath in tests/test_logcr.py).  liboracle_cr.so is therefore the
+ * bitwise oracle for the GPU FAITHFUL kernels, and differs from liboracle.so
+ * only where glibc's log is misrounded.                                      */
+#ifdef FDG_ORACLE_LOGCR
+#include "../paper_2112_10517_b200/csrc/fdg_logcr.h"
+#define OR_LOG(x) log_cr(x)
+#else
+#define OR_LOG(x) log(x)
+#endif
+
 enum { F_CENTRAL = 0, F_SHIMA = 1, F_RANOCHA = 2, F_KG = 3, F_CHANDRASHEKAR = 4, F_LLF = 5, F_HLL = 6 };
 enum { PRE_NONE = 0, PRE_PRIMITIVES = 1, PRE_LOGS = 2 };
 
@@ -82,7 +95,7 @@ static inline double logmean(double a, double b)
     double u = lm_u(a, b);
     if (u < SERIES_EPSILON)
         return (a + b) / (2.0 + u * (2.0 / 3.0 + u * (2.0 / 5.0 + u * (2.0 / 7.0))));
-    return (b - a) / log(b / a);
+    return (b - a) / OR_LOG(b / a);
 }
 
 static inline double inv_logmean(double a, double b)
@@ -90,7 +103,7 @@ static inline double inv_logmean(double a, double b)
     double u = lm_u(a, b);
     if (u < SERIES_EPSILON)
         return (2.0 + u * (2.0 / 3.0 + u * (2.0 / 5.0 + u * (2.0 / 7.0)))) / (a + b);
-    return log(b / a) / (b - a);
+    return OR_LOG(b / a) / (b - a);
 }
 
 static inline double logmean_logs(double a, double b, double la, double lb)
@@ -128,8 +141,8 @@ static inline void make_node(node_t *q, const double *u, int d, double gm1, int 
     q->p = gm1 * (u[d + 1] - 0.5 * u[0] * s);
     q->x0 = q->x1 = 0.0;
     if (flux == F_RANOCHA && pre == PRE_LOGS) {
-        q->x0 = log(q->rho);
-        q->x1 = log(q->p);
+        q->x0 = OR_LOG(q->rho);
+        q->x1 = OR_LOG(q->p);
     } else if (flux == F_CHANDRASHEKAR) {
         q->x0 = q->rho / (2.0 * q->p); /* beta */
     } else if (flux == F_KG) {
@@ -446,11 +459,11 @@ static void face_normal(const or_mesh *M, int64_t owner, int n, int m, double *n
 {
     /* face_ja[n][owner, m] = owner's own Ja^n at its +face node (geometry.py:311-326) */
     const int d = M->d, p1 = M->p1, nn = ipow(p1, d);
-    if (owner < 0) {
+    if (M->cartesian) {
+        for (int j = 0; j < d; ++j) nrm[j] = (j == n) ? M->areas[n] : 0.0;
+    } else if (owner < 0) {
         const double *g = M->ghost_nrm + ((-owner - 1) * ipow(p1, d - 1) + m) * d;
         for (int j = 0; j < d; ++j) nrm[j] = g[j];
-    } else if (M->cartesian) {
-        for (int j = 0; j < d; ++j) nrm[j] = (j == n) ? M->areas[n] : 0.0;
     } else {
         int node = line_node(d, p1, n, m, p1 - 1);
         const double *src = M->ja + ((owner * nn + node) * d + n) * d;

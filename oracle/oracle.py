@@ -34,7 +34,10 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liboracle.so")
+LIB_PATHS = {
+    "glibc": os.path.join(HERE, "liboracle.so"),  # reference arithmetic, bit for bit
+    "cr": os.path.join(HERE, "liboracle_cr.so"),  # same, with the correctly rounded log_cr
+}
 
 FLUX_IDS = {
     "central": 0,
@@ -69,22 +72,22 @@ class OrMesh(ctypes.Structure):
     ]
 
 
-_lib = None
+_libs = {}
 
 
 def build(force=False):
-    """Compile liboracle.so in place (gcc, strict IEEE flags, see Makefile)."""
-    if force or not os.path.exists(LIB_PATH):
+    """Compile liboracle*.so in place (gcc, strict IEEE flags, see Makefile)."""
+    if force or not all(os.path.exists(p) for p in LIB_PATHS.values()):
         subprocess.run(["make", "-s", "-C", HERE], check=True)
-    return LIB_PATH
+    return LIB_PATHS
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+def lib(variant="glibc"):
+    if variant not in _libs:
+        path = LIB_PATHS[variant]
+        if not os.path.exists(path):
             build()
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         P = ctypes.POINTER(OrMesh)
         vp = ctypes.c_void_p
         L.or_volume.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
@@ -102,8 +105,8 @@ def lib():
         L.or_inv_logmean.argtypes = [ctypes.c_double, ctypes.c_double]
         L.or_inv_logmean.restype = ctypes.c_double
         L.or_max_threads.restype = ctypes.c_int
-        _lib = L
-    return _lib
+        _libs[variant] = L
+    return _libs[variant]
 
 
 def _ptr(a):
@@ -168,21 +171,21 @@ def _mesh(m):
     return m if isinstance(m, MeshArrays) else mesh_from_setup(m)
 
 
-def volume(u, setup, flux="ranocha", precompute="none", nthreads=0):
+def volume(u, setup, flux="ranocha", precompute="none", nthreads=0, variant="glibc"):
     m = _mesh(setup)
     u = np.ascontiguousarray(u, dtype=np.float64)
     out = np.empty_like(u)
-    lib().or_volume(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], PRE_IDS[precompute], nthreads)
+    lib(variant).or_volume(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], PRE_IDS[precompute], nthreads)
     return out
 
 
-def surface(u, setup, flux="llf", out=None, nthreads=0):
+def surface(u, setup, flux="llf", out=None, nthreads=0, variant="glibc"):
     m = _mesh(setup)
     u = np.ascontiguousarray(u, dtype=np.float64)
     if out is None:
         out = np.zeros_like(u)
     assert out.flags.c_contiguous and out.dtype == np.float64
-    lib().or_surface(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], nthreads)
+    lib(variant).or_surface(ctypes.byref(m.struct), _ptr(u), _ptr(out), FLUX_IDS[flux], nthreads)
     return out
 
 
@@ -203,7 +206,8 @@ def gate(u, setup):
     return int(g // nn), int(g % nn), float(rho[0]), float(p[0])
 
 
-def rhs(u, setup, volume_flux="ranocha", surface_flux="ranocha", precompute="none", nthreads=0):
+def rhs(u, setup, volume_flux="ranocha", surface_flux="ranocha", precompute="none", nthreads=0,
+        variant="glibc"):
     m = _mesh(setup)
     u = np.ascontiguousarray(u, dtype=np.float64)
     bad = gate(u, m)
@@ -213,21 +217,21 @@ def rhs(u, setup, volume_flux="ranocha", surface_flux="ranocha", precompute="non
             "inadmissible state at element %d, node %d: rho=%r, p=%r" % (e, i, rho, p)
         )
     du = np.empty_like(u)
-    lib().or_rhs(
+    lib(variant).or_rhs(
         ctypes.byref(m.struct), _ptr(u), _ptr(du), FLUX_IDS[volume_flux], FLUX_IDS[surface_flux],
         PRE_IDS[precompute], nthreads,
     )
     return du
 
 
-def two_point(ul, ur, normal, flux, gamma=1.4, cart_axis=-1, precompute="none"):
+def two_point(ul, ur, normal, flux, gamma=1.4, cart_axis=-1, precompute="none", variant="glibc"):
     ul = np.ascontiguousarray(ul, dtype=np.float64)
     ur = np.ascontiguousarray(ur, dtype=np.float64)
     nrm = np.zeros(3)
     nrm[: len(normal)] = normal
     f = np.zeros(5)
     d = ul.shape[0] - 2
-    lib().or_two_point(d, FLUX_IDS[flux], PRE_IDS[precompute], gamma, 1.0 / (gamma - 1.0),
+    lib(variant).or_two_point(d, FLUX_IDS[flux], PRE_IDS[precompute], gamma, 1.0 / (gamma - 1.0),
                        _ptr(ul), _ptr(ur), _ptr(nrm), cart_axis, _ptr(f))
     return f[: d + 2]
 

@@ -1,0 +1,150 @@
+"""ctypes binding of libfdg.so (include/fdg.h).
+
+The product path has no CPU fallback: if the library is missing or fails to
+load, every entry point raises NativeLibraryError.
+"""
+
+import ctypes
+import os
+
+from .errors import ConfigurationError, NativeLibraryError, UnsupportedOperatorError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfdg.so")
+
+FLUX_IDS = {
+    "central": 0,
+    "shima": 1,
+    "ranocha": 2,
+    "kennedy_gruber": 3,
+    "chandrashekar": 4,
+    "llf": 5,
+    "hll": 6,
+}
+PRECOMPUTE_IDS = {"none": 0, "primitives": 1, "primitives_and_logs": 2}
+MODE_IDS = {"reference": 0, "batched": 1}  # RhsConfig.kernel -> FAITHFUL / FAST
+
+FDG_OK, FDG_ERR_CONFIG, FDG_ERR_UNSUPPORTED, FDG_ERR_CUDA, FDG_ERR_ARG = range(5)
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("degree", ctypes.c_int32),
+        ("n_elem", ctypes.c_int64),
+        ("elem_base", ctypes.c_int64),
+        ("gamma", ctypes.c_double),
+        ("inv_gamma_minus_one", ctypes.c_double),
+        ("dsplit", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("cartesian", ctypes.c_int32),
+        ("areas", ctypes.c_double * 3),
+        ("jac_const", ctypes.c_double),
+        ("ja", ctypes.c_void_p),
+        ("jac", ctypes.c_void_p),
+        ("plus", ctypes.c_void_p),
+        ("minus", ctypes.c_void_p),
+        ("ghost_nrm", ctypes.c_void_p),
+    ]
+
+
+class Scheme(ctypes.Structure):
+    _fields_ = [
+        ("volume_flux", ctypes.c_int32),
+        ("surface_flux", ctypes.c_int32),
+        ("precompute", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+    ]
+
+
+class Stage(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("index", ctypes.c_uint32),
+        ("a", ctypes.c_double),
+        ("b", ctypes.c_double),
+        ("cdt", ctypes.c_double),
+        ("dt", ctypes.c_double),
+    ]
+
+
+class StatusRec(ctypes.Structure):
+    _fields_ = [("first_bad", ctypes.c_int64), ("bad_stage", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+EXPORTS = (
+    "fdg_abi_version",
+    "fdg_last_error",
+    "fdg_supported",
+    "fdg_launch_count",
+    "fdg_mesh_create",
+    "fdg_mesh_destroy",
+    "fdg_volume",
+    "fdg_surface",
+    "fdg_rhs",
+    "fdg_rk_stage",
+    "fdg_gate",
+    "fdg_reset_status",
+    "fdg_read_status",
+    "fdg_pack_faces",
+    "fdg_fp64_probe",
+)
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryError(
+            "libfdg.so not found at %s; build it with `python -c \"import __graft_entry__ as g; g.build()\"`"
+            % LIB_PATH
+        )
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as err:
+        raise NativeLibraryError("libfdg.so failed to load: %s" % err) from err
+    vp, i32, P = ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER
+    L.fdg_abi_version.restype = ctypes.c_int
+    L.fdg_last_error.restype = ctypes.c_char_p
+    L.fdg_supported.argtypes = [i32, i32]
+    L.fdg_launch_count.restype = ctypes.c_ulonglong
+    L.fdg_mesh_create.argtypes = [P(MeshDesc), P(vp)]
+    L.fdg_mesh_destroy.argtypes = [vp]
+    L.fdg_mesh_destroy.restype = None
+    L.fdg_volume.argtypes = [vp, P(Scheme), vp, vp, vp]
+    L.fdg_surface.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
+    L.fdg_rhs.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
+    L.fdg_rk_stage.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, vp]
+    L.fdg_gate.argtypes = [vp, vp, vp]
+    L.fdg_reset_status.argtypes = [vp, vp]
+    L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]
+    L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]
+    L.fdg_fp64_probe.argtypes = [P(ctypes.c_double), vp]
+    if L.fdg_abi_version() != 1:
+        raise NativeLibraryError("libfdg.so ABI version %d, expected 1" % L.fdg_abi_version())
+    _lib = L
+    return L
+
+
+def check(rc):
+    if rc == FDG_OK:
+        return
+    msg = lib().fdg_last_error().decode("utf-8", "replace")
+    if rc == FDG_ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if rc == FDG_ERR_UNSUPPORTED:
+        raise UnsupportedOperatorError(msg)
+    raise NativeLibraryError(msg)
+
+
+def launch_count():
+    return int(lib().fdg_launch_count())
+
+
+def fp64_peak_tflops(stream=None):
+    out = ctypes.c_double(0.0)
+    check(lib().fdg_fp64_probe(ctypes.byref(out), stream))
+    return out.value

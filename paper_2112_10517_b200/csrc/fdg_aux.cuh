@@ -1,0 +1,43 @@
+// fdg_aux.cuh -- small non-template kernels (halo packing, standalone gate);
+// included by exactly one translation unit (fdg_capi.cu).
+#pragma once
+#include "fdg_kernels.cuh"
+
+namespace fdg {
+
+// Gather the face traces of `n_list` elements (halo send buffers): out[(i, m, v)]
+// = u[list[i], line_node(dir, m, pos), v] for pos = 0 (side 0) or p (side 1).
+__global__ void pack_faces_kernel(const double* __restrict__ u, const int* __restrict__ list, int n_list, int d,
+                                  int p1, int dir, int side, double* __restrict__ out)
+{
+    const int nvar = d + 2;
+    int fn = 1;
+    for (int i = 0; i < d - 1; ++i) fn *= p1;
+    int nn = fn * p1;
+    int stride = 1;
+    for (int i = 0; i < d - 1 - dir; ++i) stride *= p1;
+    const int pos = side ? p1 - 1 : 0;
+    const long long total = (long long)n_list * fn * nvar;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int v = (int)(t % nvar);
+        const long long im = t / nvar;
+        const int mm = (int)(im % fn);
+        const long long i = im / fn;
+        const int node = (mm / stride * p1 + pos) * stride + mm % stride;
+        out[t] = u[((long long)list[i] * nn + node) * nvar + v];
+    }
+}
+
+// Standalone admissibility gate (discretization.py:660-672).
+template <int D>
+__global__ void gate_kernel(const double* __restrict__ u, long long n_nodes, double gm1, long long node_base,
+                            Status* status)
+{
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_nodes;
+         t += (long long)gridDim.x * blockDim.x) {
+        if (!gate_ok<D>(u + t * (D + 2), gm1)) atomicMin(&status->first_bad, (unsigned long long)(node_base + t));
+    }
+}
+
+}  // namespace fdg

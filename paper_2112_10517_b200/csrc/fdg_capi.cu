@@ -1,0 +1,299 @@
+// fdg_capi.cu -- the extern "C" boundary of libfdg.so (declared in include/fdg.h).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fdg.h"
+#include "fdg_aux.cuh"
+#include "fdg_dispatch.cuh"
+
+using namespace fdg;
+
+struct fdg_mesh {
+    int d = 0, p1 = 0;
+    long long n_elem = 0;
+    bool curved = false;
+    int sm_count = 148;
+    KParams base{};
+    Status* status = nullptr;  // device
+};
+
+static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+static int fail(int rc, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int rc, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return rc;
+}
+
+static int cuda_fail(cudaError_t err, const char* what)
+{
+    return fail(FDG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(err));
+}
+
+static const char* flux_name(int k)
+{
+    static const char* names[] = {"central", "shima", "ranocha", "kennedy_gruber", "chandrashekar", "llf", "hll"};
+    return (k >= 0 && k < 7) ? names[k] : "?";
+}
+
+extern "C" {
+
+int fdg_abi_version(void) { return FDG_ABI_VERSION; }
+
+const char* fdg_last_error(void) { return g_last_error.c_str(); }
+
+int fdg_supported(int32_t d, int32_t degree) { return (d == 2 || d == 3) && degree >= 1 && degree <= 7; }
+
+unsigned long long fdg_launch_count(void) { return g_launches.load(); }
+
+int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
+{
+    if (!desc || !out) return fail(FDG_ERR_ARG, "fdg_mesh_create: null argument");
+    *out = nullptr;
+    if (desc->d != 2 && desc->d != 3)
+        return fail(FDG_ERR_UNSUPPORTED, "supported dimensions are 2 and 3, got %d", desc->d);
+    if (desc->degree < 1 || desc->degree > 7)
+        return fail(FDG_ERR_UNSUPPORTED, "degree %d outside the device-supported range 1..7", desc->degree);
+    if (desc->n_elem < 0) return fail(FDG_ERR_ARG, "n_elem must be >= 0");
+    if (!desc->dsplit || !desc->weights) return fail(FDG_ERR_ARG, "dsplit and weights are required");
+    if (!desc->plus || !desc->minus) return fail(FDG_ERR_ARG, "neighbour tables are required");
+    if (!desc->cartesian && (!desc->ja || !desc->jac))
+        return fail(FDG_ERR_ARG, "curved meshes need device ja and jac");
+    fdg_mesh* m = new fdg_mesh();
+    m->d = desc->d;
+    m->p1 = desc->degree + 1;
+    m->n_elem = desc->n_elem;
+    m->curved = !desc->cartesian;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    KParams& k = m->base;
+    memset(&k, 0, sizeof(k));
+    for (int i = 0; i < m->p1 * m->p1; ++i) k.dsplit[i] = desc->dsplit[i];
+    k.w0 = desc->weights[0];
+    k.wp = desc->weights[m->p1 - 1];
+    for (int i = 0; i < 3; ++i) k.areas[i] = desc->areas[i];
+    k.jac_const = desc->jac_const;
+    k.ja = desc->ja;
+    k.jac = desc->jac;
+    k.plus = desc->plus;
+    k.minus = desc->minus;
+    k.ghost_nrm = desc->ghost_nrm;
+    k.n_elem = desc->n_elem;
+    k.elem_base = desc->elem_base;
+    k.gas.gamma = desc->gamma;
+    k.gas.gm1 = desc->gamma - 1.0;  // fluxes.py: gm1 = gas.gamma - 1.0
+    k.gas.igm1 = desc->inv_gamma_minus_one;
+    cudaError_t err = cudaMalloc(&m->status, sizeof(Status));
+    if (err != cudaSuccess) {
+        delete m;
+        return cuda_fail(err, "cudaMalloc(status)");
+    }
+    err = cudaMemset(m->status, 0xff, sizeof(Status));
+    if (err != cudaSuccess) {
+        cudaFree(m->status);
+        delete m;
+        return cuda_fail(err, "cudaMemset(status)");
+    }
+    k.status = m->status;
+    *out = m;
+    return FDG_OK;
+}
+
+void fdg_mesh_destroy(fdg_mesh_t* m)
+{
+    if (!m) return;
+    if (m->status) cudaFree(m->status);
+    delete m;
+}
+
+static int check_scheme(const fdg_scheme_t* s, bool need_volume, bool need_surface)
+{
+    if (!s) return fail(FDG_ERR_ARG, "scheme is null");
+    if (s->mode != FDG_MODE_FAITHFUL && s->mode != FDG_MODE_FAST)
+        return fail(FDG_ERR_CONFIG, "kernel: unknown mode %d", s->mode);
+    if (s->precompute < 0 || s->precompute > 2)
+        return fail(FDG_ERR_CONFIG, "precompute: unknown mode %d", s->precompute);
+    if (need_volume && (s->volume_flux < 0 || s->volume_flux > F_CHANDRASHEKAR))
+        return fail(FDG_ERR_CONFIG,
+                    "volume flux must be symmetric (central, shima, ranocha, kennedy_gruber, chandrashekar), "
+                    "got %s",
+                    flux_name(s->volume_flux));
+    if (need_surface && (s->surface_flux < 0 || s->surface_flux > F_HLL))
+        return fail(FDG_ERR_CONFIG, "surface_flux: unknown kind %d", s->surface_flux);
+    return FDG_OK;
+}
+
+using PickFn = LaunchFn (*)(int, bool, int);
+
+#define FDG_ROW(m, d)                                                                                    \
+    {                                                                                                    \
+        fdg_pick_##m##_d##d##_p2, fdg_pick_##m##_d##d##_p3, fdg_pick_##m##_d##d##_p4, fdg_pick_##m##_d##d##_p5, \
+            fdg_pick_##m##_d##d##_p6, fdg_pick_##m##_d##d##_p7, fdg_pick_##m##_d##d##_p8                   \
+    }
+
+static LaunchFn find(const fdg_mesh* m, const fdg_scheme_t* s, int vf)
+{
+    static const PickFn faithful[2][7] = {FDG_ROW(faithful, 2), FDG_ROW(faithful, 3)};
+    static const PickFn fast[2][7] = {FDG_ROW(fast, 2), FDG_ROW(fast, 3)};
+    if (m->p1 < 2 || m->p1 > 8 || m->d < 2 || m->d > 3) return nullptr;
+    const int logs = (s->precompute == FDG_PRE_PRIMITIVES_AND_LOGS) ? 1 : 0;
+    const PickFn fn = (s->mode == FDG_MODE_FAITHFUL ? faithful : fast)[m->d - 2][m->p1 - 2];
+    return fn(vf, m->curved, logs);
+}
+
+static int run(fdg_mesh* m, const fdg_scheme_t* s, KParams& k, int vf, void* stream)
+{
+    LaunchFn fn = find(m, s, vf);
+    if (!fn) return fail(FDG_ERR_UNSUPPORTED, "no kernel for d=%d, p=%d, flux %s", m->d, m->p1 - 1, flux_name(vf));
+    if (m->n_elem == 0) return FDG_OK;
+    cudaError_t err = fn(k, (cudaStream_t)stream, m->sm_count);
+    if (err != cudaSuccess) return cuda_fail(err, "element kernel launch");
+    g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_volume(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, double* vol, void* stream)
+{
+    if (!m || !u || !vol) return fail(FDG_ERR_ARG, "fdg_volume: null argument");
+    int rc = check_scheme(s, true, false);
+    if (rc) return rc;
+    KParams k = m->base;
+    k.u = u;
+    k.out = vol;
+    k.epilogue = EPI_VOLUME;
+    k.precompute = s->precompute;
+    k.surface_flux = F_LLF;
+    return run(m, s, k, s->volume_flux, stream);
+}
+
+int fdg_surface(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* out,
+                void* stream)
+{
+    if (!m || !u || !out) return fail(FDG_ERR_ARG, "fdg_surface: null argument");
+    int rc = check_scheme(s, false, true);
+    if (rc) return rc;
+    KParams k = m->base;
+    k.u = u;
+    k.out = out;
+    k.ghost_u = ghost_u;
+    k.epilogue = EPI_SURFACE;
+    k.surface_flux = s->surface_flux;
+    k.precompute = s->precompute;
+    // the surface-only pass does not stage volume data: any instantiation works
+    return run(m, s, k, F_SHIMA, stream);
+}
+
+int fdg_rhs(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* du,
+            void* stream)
+{
+    if (!m || !u || !du) return fail(FDG_ERR_ARG, "fdg_rhs: null argument");
+    if (u == du) return fail(FDG_ERR_ARG, "fdg_rhs: du must not alias u");
+    int rc = check_scheme(s, true, true);
+    if (rc) return rc;
+    KParams k = m->base;
+    k.u = u;
+    k.out = du;
+    k.ghost_u = ghost_u;
+    k.epilogue = EPI_RHS;
+    k.surface_flux = s->surface_flux;
+    k.precompute = s->precompute;
+    return run(m, s, k, s->volume_flux, stream);
+}
+
+int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, const double* v_in,
+                 const double* ghost_u, double* v_out, double* reg, const double* u0, void* stream)
+{
+    if (!m || !st || !v_in || !v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: null argument");
+    if (v_in == v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: v_out must not alias v_in");
+    if (st->kind == 0 && !reg) return fail(FDG_ERR_ARG, "fdg_rk_stage: 2N stage needs the register");
+    if (st->kind == 1 && st->a != 0.0 && !u0) return fail(FDG_ERR_ARG, "fdg_rk_stage: stage needs u0");
+    if (st->kind != 0 && st->kind != 1) return fail(FDG_ERR_CONFIG, "stage kind %d unknown", st->kind);
+    int rc = check_scheme(s, true, true);
+    if (rc) return rc;
+    KParams k = m->base;
+    k.u = v_in;
+    k.out = v_out;
+    k.ghost_u = ghost_u;
+    k.reg = reg;
+    k.u0 = u0;
+    k.epilogue = EPI_STAGE;
+    k.surface_flux = s->surface_flux;
+    k.precompute = s->precompute;
+    k.stage_kind = st->kind;
+    k.stage_index = st->index;
+    k.sa = st->a;
+    k.sb = st->b;
+    k.sc = st->cdt;
+    k.dt = st->dt;
+    return run(m, s, k, s->volume_flux, stream);
+}
+
+int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)
+{
+    if (!m || !u) return fail(FDG_ERR_ARG, "fdg_gate: null argument");
+    long long nn = 1;
+    for (int i = 0; i < m->d; ++i) nn *= m->p1;
+    const long long n_nodes = m->n_elem * nn;
+    if (n_nodes == 0) return FDG_OK;
+    const int threads = 256;
+    const long long blocks = std::min<long long>((n_nodes + threads - 1) / threads, (long long)m->sm_count * 16);
+    const double gm1 = m->base.gas.gm1;
+    const long long node_base = m->base.elem_base * nn;
+    if (m->d == 2)
+        gate_kernel<2><<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(u, n_nodes, gm1, node_base, m->status);
+    else
+        gate_kernel<3><<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(u, n_nodes, gm1, node_base, m->status);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "gate kernel launch");
+    g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_reset_status(fdg_mesh_t* m, void* stream)
+{
+    if (!m) return fail(FDG_ERR_ARG, "fdg_reset_status: null mesh");
+    cudaError_t err = cudaMemsetAsync(m->status, 0xff, sizeof(Status), (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync(status)");
+    return FDG_OK;
+}
+
+int fdg_read_status(fdg_mesh_t* m, fdg_status_t* out, void* stream)
+{
+    if (!m || !out) return fail(FDG_ERR_ARG, "fdg_read_status: null argument");
+    Status h;
+    cudaError_t err = cudaMemcpyAsync(&h, m->status, sizeof(Status), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize((cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "status read");
+    out->first_bad = (h.first_bad == ~0ULL) ? -1 : (int64_t)h.first_bad;
+    out->bad_stage = (h.bad_stage == ~0U) ? -1 : (int32_t)h.bad_stage;
+    out->pad = 0;
+    return FDG_OK;
+}
+
+int fdg_pack_faces(const double* u, const int32_t* elems, int32_t n, int32_t d, int32_t degree, int32_t dir,
+                   int32_t side, double* out, void* stream)
+{
+    if (!u || !elems || !out) return fail(FDG_ERR_ARG, "fdg_pack_faces: null argument");
+    if ((d != 2 && d != 3) || degree < 1 || dir < 0 || dir >= d) return fail(FDG_ERR_ARG, "fdg_pack_faces: bad shape");
+    if (n == 0) return FDG_OK;
+    const int threads = 256;
+    const int blocks = 296;
+    pack_faces_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(u, elems, n, d, degree + 1, dir, side, out);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "pack kernel launch");
+    g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+}  // extern "C"

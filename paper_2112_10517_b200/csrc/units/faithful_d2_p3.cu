@@ -1,0 +1,7 @@
+// instantiation unit: mode FAITHFUL, d = 2, p + 1 = 3 (compiled with --fmad=false)
+#include "../fdg_dispatch.cuh"
+
+fdg::LaunchFn fdg_pick_faithful_d2_p3(int vf, bool curved, int logs)
+{
+    return fdg::pick_flux<2, 3, fdg::FAITHFUL>(vf, curved, logs);
+}

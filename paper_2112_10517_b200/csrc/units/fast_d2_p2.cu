@@ -1,0 +1,7 @@
+// instantiation unit: mode FAST, d = 2, p + 1 = 2
+#include "../fdg_dispatch.cuh"
+
+fdg::LaunchFn fdg_pick_fast_d2_p2(int vf, bool curved, int logs)
+{
+    return fdg::pick_flux<2, 2, fdg::FAST>(vf, curved, logs);
+}

@@ -1,0 +1,7 @@
+// instantiation unit: mode FAST, d = 2, p + 1 = 8
+#include "../fdg_dispatch.cuh"
+
+fdg::LaunchFn fdg_pick_fast_d2_p8(int vf, bool curved, int logs)
+{
+    return fdg::pick_flux<2, 8, fdg::FAST>(vf, curved, logs);
+}

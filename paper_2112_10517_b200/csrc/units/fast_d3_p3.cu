@@ -1,0 +1,7 @@
+// instantiation unit: mode FAST, d = 3, p + 1 = 3
+#include "../fdg_dispatch.cuh"
+
+fdg::LaunchFn fdg_pick_fast_d3_p3(int vf, bool curved, int logs)
+{
+    return fdg::pick_flux<3, 3, fdg::FAST>(vf, curved, logs);
+}

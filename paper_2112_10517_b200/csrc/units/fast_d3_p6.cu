@@ -1,0 +1,7 @@
+// instantiation unit: mode FAST, d = 3, p + 1 = 6
+#include "../fdg_dispatch.cuh"
+
+fdg::LaunchFn fdg_pick_fast_d3_p6(int vf, bool curved, int logs)
+{
+    return fdg::pick_flux<3, 6, fdg::FAST>(vf, curved, logs);
+}

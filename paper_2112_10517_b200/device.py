@@ -1,0 +1,246 @@
+"""Device image of a SpatialSetup and the stream-ordered calls into libfdg.so.
+
+PyTorch is used only to own device memory and streams; all arithmetic runs in
+the sm_100a kernels behind include/fdg.h. A DeviceMesh accepts either this
+package's SpatialSetup or the reference's (duck-typed: d, op.weights,
+op.degree, dsplit.matrix, metrics.{cartesian, ja, jac}, plus_neighbor, gas).
+"""
+
+import ctypes
+import weakref
+
+import numpy as np
+
+from . import _native as N
+from .errors import AdmissibilityError, ConfigurationError, DivergenceError, UnsupportedOperatorError
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import NativeLibraryError
+
+        raise NativeLibraryError("no CUDA device: the flux-differencing path runs on the GPU only")
+    return torch
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def scheme_struct(volume_flux, surface_flux, precompute, kernel):
+    try:
+        return N.Scheme(
+            N.FLUX_IDS[volume_flux] if volume_flux is not None else 1,
+            N.FLUX_IDS[surface_flux] if surface_flux is not None else 5,
+            N.PRECOMPUTE_IDS[precompute],
+            N.MODE_IDS[kernel],
+        )
+    except KeyError as err:
+        raise ConfigurationError("unknown scheme option %s" % err) from err
+
+
+def _metric_scalars(metrics, d):
+    """(areas, J) of a Cartesian mesh from either metrics flavour."""
+    areas = getattr(metrics, "areas", None)
+    jac_const = getattr(metrics, "jac_const", None)
+    if areas is None or jac_const is None:
+        ja0 = np.asarray(metrics.ja[0, 0])
+        areas = tuple(float(ja0[n, n]) for n in range(d))
+        jac_const = float(metrics.jac[0, 0])
+    return tuple(areas), float(jac_const)
+
+
+class DeviceMesh:
+    """Uploaded tables + the libfdg mesh handle for one (partition of a) mesh.
+
+    ``partition`` (optional) describes a slab of a larger mesh: a dict with
+    ``lo``/``hi`` (global element range), ``plus``/``minus`` (d, n_local) int
+    neighbour tables where negative entries are ghost slots, and
+    ``ghost_nrm`` (n_ghost, fn, d) face normals for curved meshes
+    (see parallel.py).
+    """
+
+    def __init__(self, setup, device=None, partition=None):
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        self.d = int(setup.d)
+        op = setup.op
+        self.degree = int(op.degree)
+        self.p1 = self.degree + 1
+        self.nn = self.p1**self.d
+        self.nvar = self.d + 2
+        self.fn = self.p1 ** (self.d - 1)
+        if not N.lib().fdg_supported(self.d, self.degree):
+            raise UnsupportedOperatorError(
+                "degree %d in %dD is outside the device kernels' range (p = 1..7)" % (self.degree, self.d)
+            )
+        gas = setup.gas
+        self.gamma = float(gas.gamma)
+        metrics = setup.metrics
+        self.cartesian = bool(metrics.cartesian)
+        dsplit = np.ascontiguousarray(np.asarray(setup.dsplit.matrix, dtype=np.float64))
+        weights = np.ascontiguousarray(np.asarray(op.weights, dtype=np.float64))
+        self._host_keep = (dsplit, weights)
+        if partition is None:
+            plus = np.stack([np.asarray(setup.plus_neighbor[n], dtype=np.int64) for n in range(self.d)])
+            n_elem = plus.shape[1]
+            minus = np.empty_like(plus)
+            for n in range(self.d):
+                minus[n, plus[n]] = np.arange(n_elem)
+            lo, hi = 0, n_elem
+            ghost_nrm = None
+        else:
+            plus = np.asarray(partition["plus"], dtype=np.int64)
+            minus = np.asarray(partition["minus"], dtype=np.int64)
+            lo, hi = int(partition["lo"]), int(partition["hi"])
+            n_elem = hi - lo
+            ghost_nrm = partition.get("ghost_nrm")
+        self.n_elem, self.elem_lo = n_elem, lo
+        dev = self.device
+        self.plus = torch.as_tensor(plus.astype(np.int32), device=dev).contiguous()
+        self.minus = torch.as_tensor(minus.astype(np.int32), device=dev).contiguous()
+        self.ja = self.jac = self.ghost_nrm = None
+        areas, jac_const = (0.0, 0.0, 0.0), 0.0
+        if self.cartesian:
+            areas, jac_const = _metric_scalars(metrics, self.d)
+            areas = tuple(areas) + (0.0,) * (3 - len(areas))
+        else:
+            self.ja = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.ja)[lo:hi]), device=dev)
+            self.jac = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.jac)[lo:hi]), device=dev)
+            if ghost_nrm is not None:
+                self.ghost_nrm = torch.as_tensor(np.ascontiguousarray(ghost_nrm, dtype=np.float64), device=dev)
+        desc = N.MeshDesc()
+        desc.d, desc.degree, desc.n_elem, desc.elem_base = self.d, self.degree, n_elem, lo
+        desc.gamma, desc.inv_gamma_minus_one = float(gas.gamma), float(gas.inv_gamma_minus_one)
+        desc.dsplit, desc.weights = dsplit.ctypes.data, weights.ctypes.data
+        desc.cartesian = int(self.cartesian)
+        desc.areas = (ctypes.c_double * 3)(*areas)
+        desc.jac_const = jac_const
+        desc.ja = None if self.ja is None else self.ja.data_ptr()
+        desc.jac = None if self.jac is None else self.jac.data_ptr()
+        desc.plus, desc.minus = self.plus.data_ptr(), self.minus.data_ptr()
+        desc.ghost_nrm = None if self.ghost_nrm is None else self.ghost_nrm.data_ptr()
+        handle = ctypes.c_void_p()
+        N.check(N.lib().fdg_mesh_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self.handle = handle
+        self._finalizer = weakref.finalize(self, N.lib().fdg_mesh_destroy, handle)
+        self.areas, self.jac_const = areas[: self.d], jac_const
+        self._staging = {}
+
+    # ------------------------------------------------------------ shapes
+    @property
+    def shape(self):
+        return (self.n_elem, self.nn, self.nvar)
+
+    def empty(self):
+        return self.torch.empty(self.shape, dtype=self.torch.float64, device=self.device)
+
+    def staging(self, key, shape):
+        """Pinned host buffer reused across calls (no allocation on the hot path)."""
+        buf = self._staging.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = self.torch.empty(shape, dtype=self.torch.float64, pin_memory=True)
+            self._staging[key] = buf
+        return buf
+
+    # ------------------------------------------------------------- calls
+    def volume(self, u, scheme, out=None, stream=None):
+        out = self.empty() if out is None else out
+        N.check(N.lib().fdg_volume(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(out), _stream_handle(stream)))
+        return out
+
+    def surface(self, u, scheme, out, ghost_u=None, stream=None):
+        N.check(
+            N.lib().fdg_surface(
+                self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out), _stream_handle(stream)
+            )
+        )
+        return out
+
+    def rhs(self, u, scheme, out=None, ghost_u=None, stream=None):
+        out = self.empty() if out is None else out
+        N.check(
+            N.lib().fdg_rhs(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out), _stream_handle(stream))
+        )
+        return out
+
+    def stage(self, scheme, stage, v_in, v_out, reg=None, u0=None, ghost_u=None, stream=None):
+        N.check(
+            N.lib().fdg_rk_stage(
+                self.handle,
+                ctypes.byref(scheme),
+                ctypes.byref(stage),
+                _ptr(v_in),
+                _ptr(ghost_u),
+                _ptr(v_out),
+                _ptr(reg),
+                _ptr(u0),
+                _stream_handle(stream),
+            )
+        )
+        return v_out
+
+    def gate(self, u, stream=None):
+        N.check(N.lib().fdg_gate(self.handle, _ptr(u), _stream_handle(stream)))
+
+    def reset_status(self, stream=None):
+        N.check(N.lib().fdg_reset_status(self.handle, _stream_handle(stream)))
+
+    def read_status(self, stream=None):
+        rec = N.StatusRec()
+        N.check(N.lib().fdg_read_status(self.handle, ctypes.byref(rec), _stream_handle(stream)))
+        return int(rec.first_bad), int(rec.bad_stage)
+
+    def pack_faces(self, u, elems, direction, side, out, stream=None):
+        N.check(
+            N.lib().fdg_pack_faces(
+                _ptr(u), _ptr(elems), int(elems.numel()), self.d, self.degree, direction, side, _ptr(out),
+                _stream_handle(stream),
+            )
+        )
+        return out
+
+    # ------------------------------------------------------------ errors
+    def raise_if_inadmissible(self, u, first_bad, gamma):
+        """AdmissibilityError with the reference gate's message
+        (discretization.py:668-671); indices are global element ids."""
+        if first_bad < 0:
+            return
+        e, i = divmod(first_bad, self.nn)
+        row = u[e - self.elem_lo, i].double().cpu().numpy() if hasattr(u, "cpu") else np.asarray(u[e - self.elem_lo, i])
+        rho = row[0]
+        mom = row[1 : self.d + 1]
+        p = (gamma - 1.0) * (row[self.d + 1] - 0.5 * np.sum(mom * mom, axis=-1) / rho)
+        raise AdmissibilityError(
+            "inadmissible state at element %d, node %d: rho=%r, p=%r" % (int(e), int(i), float(rho), float(p))
+        )
+
+
+_CACHE = {}
+
+
+def device_mesh_for(setup, device=None):
+    """DeviceMesh cached per setup object (weakly; rebuilt if the setup dies)."""
+    key = (id(setup), str(device))
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0]() is setup:
+        return hit[1]
+    dm = DeviceMesh(setup, device=device)
+    try:
+        ref = weakref.ref(setup)
+    except TypeError:  # objects without weakref support: keep them alive with the cache entry
+        ref = (lambda s: (lambda: s))(setup)
+    _CACHE[key] = (ref, dm)
+    return dm
+
+
+__all__ = ["DeviceMesh", "device_mesh_for", "scheme_struct", "DivergenceError"]

@@ -1,0 +1,370 @@
+"""Drop-in RHS / volume-integral entry points (reference discretization.py and
+batched.py signatures), executed by the sm_100a kernels of libfdg.so.
+
+    rhs(u, setup, config, counter=None)            discretization.py:896-963
+    volume_fluxdiff(u_elem, dop, metrics, vol_flux, gas, pre=None)
+                                                   discretization.py:267-323
+    mesh_fluxdiff_volume(u, setup, config)         batched.py:450-511
+    mesh_surface(u, setup, surface_flux, out)      batched.py:514-544
+    surface_terms(u, setup, surface_flux, out=None)  discretization.py:681-788
+
+``RhsConfig.kernel`` keeps the reference's two names with the reference's
+meaning: "reference" is the bitwise-reproducible path (the FAITHFUL kernels:
+the scalar path's operation order, IEEE division, correctly rounded log) and
+"batched" the throughput path (the FAST kernels). Inputs may be numpy arrays
+(copied through pinned staging buffers, a new numpy array is returned, as in
+the reference) or torch tensors (CUDA tensors stay on the device; CPU tensors
+are copied in and the result copied back).
+
+``setup`` may be this package's SpatialSetup or the reference's own.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import fluxes as _fluxes
+from .device import device_mesh_for, scheme_struct
+from .errors import AdmissibilityError, ConfigurationError, UnsupportedOperatorError
+from .euler import entropy_vars
+from .geometry import compute_metrics, element_coords, neighbor_table
+from .operators import build_dsplit, node_lines, pair_table
+
+VOLUME_SCHEMES = ("fluxdiff",)
+PRECOMPUTE_MODES = ("none", "primitives", "primitives_and_logs")
+KERNELS = ("reference", "batched")
+VOLUME_KINDS = _fluxes.VOLUME_KINDS
+SURFACE_KINDS = _fluxes.SURFACE_KINDS
+_OUT_OF_SCOPE_SCHEMES = ("strong", "weak", "overintegration", "gauss_fluxdiff", "gauss_surface_correction")
+
+
+@dataclass(frozen=True)
+class RhsConfig:
+    """Scheme selection for one RHS evaluation (reference discretization.py:87-150)."""
+
+    volume_scheme: str = "fluxdiff"
+    volume_flux: str = "ranocha"
+    surface_flux: str = "ranocha"
+    precompute: str = "none"
+    overint_degree: int = None
+    kernel: str = "reference"
+
+    def validate(self, setup=None):
+        if self.volume_scheme not in VOLUME_SCHEMES:
+            if self.volume_scheme in _OUT_OF_SCOPE_SCHEMES:
+                raise ConfigurationError(
+                    "volume_scheme: %r is not on the device path (flux differencing only)" % (self.volume_scheme,)
+                )
+            raise ConfigurationError(
+                "volume_scheme: unknown scheme %r (choose from %s)" % (self.volume_scheme, ", ".join(VOLUME_SCHEMES))
+            )
+        if self.precompute not in PRECOMPUTE_MODES:
+            raise ConfigurationError(
+                "precompute: unknown mode %r (choose from %s)" % (self.precompute, ", ".join(PRECOMPUTE_MODES))
+            )
+        if self.kernel not in KERNELS:
+            raise ConfigurationError("kernel: unknown kernel %r (choose from %s)" % (self.kernel, ", ".join(KERNELS)))
+        if self.surface_flux not in SURFACE_KINDS:
+            raise ConfigurationError(
+                "surface_flux: unknown kind %r (choose from %s)" % (self.surface_flux, ", ".join(SURFACE_KINDS))
+            )
+        _fluxes.require_volume_kind(self.volume_flux)
+        if setup is not None:
+            family = getattr(setup.op, "family", "lgl")
+            if family != "lgl":
+                raise ConfigurationError(
+                    "volume_scheme: 'fluxdiff' requires the lgl family (diagonal boundary operator)"
+                )
+
+    def scheme(self):
+        return scheme_struct(self.volume_flux, self.surface_flux, self.precompute, self.kernel)
+
+
+@dataclass(frozen=True)
+class SpatialSetup:
+    """Everything precomputable for RHS evaluations on one mesh/operator
+    (reference discretization.py:576-606)."""
+
+    mesh: object
+    op: object
+    gas: object
+    metrics: object
+    coords: np.ndarray
+    lines: tuple
+    plus_neighbor: tuple
+    dsplit: object
+
+    @property
+    def n_elements(self):
+        return self.mesh.n_elements
+
+    @property
+    def n_nodes(self):
+        return self.op.n_nodes**self.mesh.d
+
+    @property
+    def d(self):
+        return self.mesh.d
+
+    @property
+    def dofs(self):
+        return self.n_elements * self.n_nodes
+
+    @property
+    def wbar(self):
+        w = np.ones(1)
+        for _ in range(self.d):
+            w = np.kron(w, self.op.weights)
+        return w
+
+
+def build_setup(mesh, op, gas, with_coords=True):
+    """Geometry, connectivity and operator tables (reference discretization.py:609-657).
+    ``with_coords=False`` skips the nodal coordinates of Cartesian meshes
+    (3.2 GB at 128^3, N=3) when no initial condition needs them."""
+    if op.family != "lgl":
+        raise UnsupportedOperatorError("the flux-differencing setup needs LGL operators, got %r" % (op.family,))
+    coords = element_coords(mesh, op) if (with_coords or not mesh.is_cartesian) else None
+    metrics = compute_metrics(mesh, op, coords)
+    return SpatialSetup(
+        mesh=mesh,
+        op=op,
+        gas=gas,
+        metrics=metrics,
+        coords=coords,
+        lines=node_lines(op.n_nodes, mesh.d),
+        plus_neighbor=neighbor_table(mesh),
+        dsplit=build_dsplit(op),
+    )
+
+
+# --------------------------------------------------------------- plumbing
+
+
+def _is_torch(x):
+    try:
+        import torch
+
+        return isinstance(x, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+class _Io:
+    """Moves a caller's array to the device and the result back in the
+    caller's flavour (numpy -> numpy, torch CPU -> torch CPU, CUDA -> CUDA)."""
+
+    def __init__(self, dm, u):
+        torch = dm.torch
+        self.dm = dm
+        self.kind = "cuda" if (_is_torch(u) and u.is_cuda) else ("torch" if _is_torch(u) else "numpy")
+        if self.kind == "cuda":
+            self.u = u if (u.dtype == torch.float64 and u.is_contiguous()) else u.double().contiguous()
+        elif self.kind == "torch" and u.dtype == torch.float64 and u.is_contiguous() and u.is_pinned():
+            # pinned caller buffer: one async H2D copy, no host staging
+            self.u = torch.empty(dm.shape, dtype=torch.float64, device=dm.device)
+            self.u.copy_(u.view(dm.shape), non_blocking=True)
+        else:
+            arr = u if _is_torch(u) else torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
+            if tuple(arr.shape) != dm.shape:
+                raise ValueError("state shape %r does not match the mesh %r" % (tuple(arr.shape), dm.shape))
+            pinned = dm.staging("in", dm.shape)
+            pinned.copy_(arr)
+            self.u = torch.empty(dm.shape, dtype=torch.float64, device=dm.device)
+            self.u.copy_(pinned, non_blocking=True)
+        if tuple(self.u.shape) != dm.shape:
+            raise ValueError("state shape %r does not match the mesh %r" % (tuple(self.u.shape), dm.shape))
+
+    def device_out(self, out=None):
+        if out is not None and _is_torch(out) and out.is_cuda:
+            return out
+        return self.dm.empty()
+
+    def finish(self, res, out=None):
+        torch = self.dm.torch
+        if out is not None and _is_torch(out):
+            if out.data_ptr() == res.data_ptr():
+                return out
+            out.copy_(res.view(out.shape), non_blocking=out.is_pinned() or out.is_cuda)
+            if not out.is_cuda:
+                torch.cuda.current_stream().synchronize()
+            return out
+        if self.kind == "cuda":
+            return res
+        pinned = self.dm.staging("out", self.dm.shape)
+        pinned.copy_(res, non_blocking=True)
+        self.dm.torch.cuda.current_stream().synchronize()
+        if self.kind == "torch":
+            if out is not None:
+                out.copy_(pinned)
+                return out
+            return pinned.clone()
+        if out is not None:
+            out[...] = pinned.numpy()
+            return out
+        return pinned.numpy().copy()
+
+
+def _count(counter, two_point, logmean):
+    _fluxes.bump(counter, two_point=two_point, logmean=logmean)
+
+
+def _volume_counts(setup, vol_flux):
+    d = setup.d
+    p1 = setup.op.degree + 1
+    n_pairs = len(pair_table(np.asarray(setup.dsplit.matrix)))
+    two_point = setup_n_elements(setup) * d * p1 ** (d - 1) * n_pairs
+    logmean = 2 * two_point if vol_flux in ("ranocha", "chandrashekar") else 0
+    return two_point, logmean
+
+
+def _surface_counts(setup):
+    d = setup.d
+    p1 = setup.op.degree + 1
+    return setup_n_elements(setup) * d * p1 ** (d - 1)
+
+
+def setup_n_elements(setup):
+    n = getattr(setup, "n_elements", None)
+    if n is not None:
+        return int(n)
+    return int(np.asarray(setup.plus_neighbor[0]).shape[0])
+
+
+def _raise_gate(dm, io, gas):
+    first_bad, _ = dm.read_status()
+    if first_bad >= 0:
+        dm.raise_if_inadmissible(io.u, first_bad, gas.gamma)
+
+
+# ------------------------------------------------------------ entry points
+
+
+def mesh_fluxdiff_volume(u, setup, config, out=None):
+    """VOL = (1/J) sum_n sum_k Dsplit f*_n  for every element (batched.py:450-511).
+    Not negated. Raises AdmissibilityError like the reference's cons2prim.
+    ``out`` (extension): a CUDA or pinned CPU tensor to receive VOL."""
+    config.validate(setup)
+    dm = device_mesh_for(setup)
+    io = _Io(dm, u)
+    dm.reset_status()
+    res = dm.volume(io.u, config.scheme(), out=io.device_out(out))
+    first_bad, _ = dm.read_status()
+    if first_bad >= 0:
+        t = io.u
+        rho = t[..., 0]
+        mom = t[..., 1 : dm.d + 1]
+        p = (setup.gas.gamma - 1.0) * (t[..., dm.d + 1] - 0.5 * rho * ((mom / rho[..., None]) ** 2).sum(-1))
+        raise AdmissibilityError(
+            "cons2prim: inadmissible state (min rho=%r, min p=%r)" % (float(rho.min()), float(p.min()))
+        )
+    tp, lm = _volume_counts(setup, config.volume_flux)
+    _count(None, tp, lm)
+    return io.finish(res, out=out)
+
+
+def mesh_surface(u, setup, surface_flux, out, kernel="batched"):
+    """out += SURF, the LGL interface terms (batched.py:514-544)."""
+    if surface_flux not in SURFACE_KINDS:
+        raise ConfigurationError("surface_flux: unknown kind %r" % (surface_flux,))
+    dm = device_mesh_for(setup)
+    io = _Io(dm, u)
+    acc = _Io(dm, out)
+    dm.surface(io.u, scheme_struct(None, surface_flux, "none", kernel), acc.u)
+    _count(None, _surface_counts(setup), 0)
+    return acc.finish(acc.u, out=out)
+
+
+def surface_terms(u, setup, surface_flux, out=None):
+    """SURF added into ``out`` (zeros if None) with the scalar path's
+    arithmetic (discretization.py:681-760, LGL branch)."""
+    if out is None:
+        out = np.zeros_like(np.asarray(u, dtype=np.float64)) if not _is_torch(u) else u.new_zeros(u.shape)
+    return mesh_surface(u, setup, surface_flux, out, kernel="reference")
+
+
+def rhs(u, setup, config, counter=None):
+    """du/dt = -(VOL + SURF) (discretization.py:896-949), admissibility gate
+    included (discretization.py:660-672)."""
+    config.validate(setup)
+    dm = device_mesh_for(setup)
+    io = _Io(dm, u)
+    dm.reset_status()
+    res = dm.rhs(io.u, config.scheme(), out=io.device_out())
+    _raise_gate(dm, io, setup.gas)
+    tp, lm = _volume_counts(setup, config.volume_flux)
+    _count(counter, tp + _surface_counts(setup), lm)
+    return io.finish(res)
+
+
+class _ElementSetup:
+    """A one-element periodic setup wrapping per-element metric terms."""
+
+    def __init__(self, dop, metrics, gas, d):
+        from types import SimpleNamespace
+
+        self.d = d
+        self.op = dop.op
+        self.dsplit = dop
+        self.gas = gas
+        ja = np.asarray(metrics.ja)
+        jac = np.asarray(metrics.jac)
+        cart = _axis_aligned_areas(ja)
+        if cart is not None:
+            self.metrics = SimpleNamespace(cartesian=True, areas=tuple(cart), jac_const=float(jac[0]), ja=ja[None], jac=jac[None])
+        else:
+            self.metrics = SimpleNamespace(cartesian=False, ja=ja[None], jac=jac[None])
+        self.plus_neighbor = tuple(np.zeros(1, dtype=np.int64) for _ in range(d))
+        self.n_elements = 1
+
+
+def _axis_aligned_areas(ja):
+    """Per-direction areas if the element's metric is constant and diagonal
+    (reference geometry.py:200-209), else None."""
+    if np.ptp(ja, axis=0).max() != 0.0:
+        return None
+    a0 = ja[0]
+    if np.count_nonzero(a0 - np.diag(np.diag(a0))):
+        return None
+    return np.diag(a0).tolist()
+
+
+def volume_fluxdiff(u_elem, dop, metrics, vol_flux, gas, pre=None):
+    """One element's VOL with the scalar path's arithmetic
+    (discretization.py:267-323). ``pre`` selects the precompute variant like
+    the reference's PrecomputedElementData (its ``mode`` is used; the tables
+    themselves are recomputed on the device)."""
+    _fluxes.require_volume_kind(vol_flux)
+    u_elem = np.asarray(u_elem, dtype=np.float64)
+    d = u_elem.shape[-1] - 2
+    mode = "none" if pre is None else getattr(pre, "mode", pre)
+    es = _ElementSetup(dop, metrics, gas, d)
+    # cache the one-element device image on the dop object's id
+    cfg = RhsConfig(volume_flux=vol_flux, precompute=mode, kernel="reference")
+    return mesh_fluxdiff_volume(u_elem[None], es, cfg)[0]
+
+
+# ------------------------------------------------------------- diagnostics
+
+
+def entropy_rate(u, dudt, setup):
+    """Normalized semidiscrete entropy production (discretization.py:1011-1024)."""
+    w = entropy_vars(u, setup.gas)
+    weights = setup.wbar[None, :] * setup.metrics.jac
+    contrib = weights * np.sum(w * dudt, axis=-1)
+    scale = np.sum(np.abs(weights[..., None] * w * dudt))
+    total = float(np.sum(contrib))
+    if scale == 0.0:
+        return 0.0, 0.0
+    return total, total / scale
+
+
+def conserved_totals(u, setup):
+    weights = setup.wbar[None, :] * setup.metrics.jac
+    return np.sum(weights[..., None] * u, axis=(0, 1))
+
+
+def error_norm_l2(u, u_exact, setup):
+    weights = setup.wbar[None, :] * setup.metrics.jac
+    diff = u - u_exact
+    return np.sqrt(np.sum(weights[..., None] * diff * diff, axis=(0, 1)))

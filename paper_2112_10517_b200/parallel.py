@@ -1,0 +1,133 @@
+"""Slab domain decomposition of the periodic mesh and the face-trace halo.
+
+One process per GPU. Rank r owns the contiguous element range of planes
+[P r / W, P (r+1) / W) of reference direction 0 (the slowest index of the
+reference's C-ordered element numbering, geometry.py:87-90), so the only data
+crossing a partition are the conserved states on the two x-faces of the slab
+(p+1)^(d-1) (d+2) doubles per face. Each side then evaluates the shared face
+flux from identical inputs (the element kernel evaluates every interface
+from both sides anyway), so the partitioned RHS is bit-identical to the
+single-domain one (tests/test_parallel.py checks it with gloo on the CPU
+oracle; the GPU path uses the same partition and buffers with NCCL).
+
+Ghost slots (negative neighbour entries -(g+1) in the local tables):
+  g in [0, F)      plus ghosts: face traces (line position 0) of the next
+                   rank's first plane, for the +x faces of my last plane
+  g in [F, 2F)     minus ghosts: face traces (line position p) of the previous
+                   rank's last plane, for the -x faces of my first plane
+with F elements per plane; ``ghost_nrm`` holds the minus neighbours' own +x
+face metrics for curved meshes (static, computed from the global setup).
+"""
+
+import numpy as np
+
+from .errors import ConfigurationError
+from .operators import node_lines
+
+
+def _plane(setup):
+    dims = setup.mesh.dims
+    n_elem = int(np.prod(dims))
+    return dims[0], n_elem // dims[0], n_elem
+
+
+def slab_partition(setup, rank, world):
+    """Local neighbour tables, ghost-slot layout and send lists of one rank."""
+    planes, F, n_elem = _plane(setup)
+    if world > planes:
+        raise ConfigurationError("cannot split %d element planes over %d ranks" % (planes, world))
+    d = setup.d
+    p1 = setup.op.degree + 1
+    p_lo, p_hi = planes * rank // world, planes * (rank + 1) // world
+    lo, hi = p_lo * F, p_hi * F
+    n_loc = hi - lo
+    plus_g = np.stack([np.asarray(setup.plus_neighbor[n], dtype=np.int64) for n in range(d)])
+    minus_g = np.empty_like(plus_g)
+    for n in range(d):
+        minus_g[n, plus_g[n]] = np.arange(n_elem)
+    plus = plus_g[:, lo:hi] - lo
+    minus = minus_g[:, lo:hi] - lo
+    if world > 1:
+        last = np.arange(hi - F, hi) - lo  # local ids of my last plane
+        first = np.arange(lo, lo + F) - lo  # local ids of my first plane
+        plus[0, last] = -(np.arange(F) + 1)
+        minus[0, first] = -(F + np.arange(F) + 1)
+    assert np.all((plus >= -2 * F) & (plus < n_loc)) and np.all((minus >= -2 * F) & (minus < n_loc))
+    ghost_nrm = None
+    if world > 1 and not setup.metrics.cartesian:
+        fn = p1 ** (d - 1)
+        ends = node_lines(p1, d)[0][:, -1]  # +x face nodes, line order
+        remote_minus = minus_g[0, lo : lo + F]  # previous rank's last plane
+        ghost_nrm = np.zeros((2 * F, fn, d))
+        ghost_nrm[F:] = np.asarray(setup.metrics.ja)[remote_minus][:, ends, 0, :]
+    return {
+        "rank": rank,
+        "world": world,
+        "lo": lo,
+        "hi": hi,
+        "plane": F,
+        "plus": plus,
+        "minus": minus,
+        "ghost_nrm": ghost_nrm,
+        "n_ghost": 2 * F if world > 1 else 0,
+        # what I send: my first plane's line-start traces to rank-1 (its plus
+        # ghosts) and my last plane's line-end traces to rank+1 (its minus ghosts)
+        "send_first": np.arange(0, F, dtype=np.int32),
+        "send_last": np.arange(n_loc - F, n_loc, dtype=np.int32),
+    }
+
+
+def pack_faces_host(u, elems, d, p1, direction, side):
+    """Host twin of fdg_pack_faces: (len(elems), fn, nvar) face traces."""
+    lines = node_lines(p1, d)[direction]
+    pos = p1 - 1 if side else 0
+    return np.ascontiguousarray(u[np.asarray(elems)][:, lines[:, pos], :])
+
+
+class HaloExchange:
+    """Face-trace exchange of one slab per RHS evaluation.
+
+    Works on CPU tensors with gloo (tests) and on CUDA tensors with NCCL;
+    ``pack`` is the device packer (DeviceMesh.pack_faces) or None for the
+    host packer. Grouped send/recv to both ring neighbours.
+    """
+
+    def __init__(self, part, d, p1, torch, dist, device="cpu", pack=None, group=None):
+        self.part, self.d, self.p1 = part, d, p1
+        self.torch, self.dist, self.group = torch, dist, group
+        self.device = device
+        self.pack = pack
+        F = part["plane"]
+        fn = p1 ** (d - 1)
+        nvar = d + 2
+        self.world, self.rank = part["world"], part["rank"]
+        mk = lambda *s: torch.empty(s, dtype=torch.float64, device=device)  # noqa: E731
+        self.send_first = mk(F, fn, nvar)
+        self.send_last = mk(F, fn, nvar)
+        self.ghost = mk(2 * F, fn, nvar)
+        self.first_idx = torch.as_tensor(part["send_first"], device=device)
+        self.last_idx = torch.as_tensor(part["send_last"], device=device)
+
+    def __call__(self, u):
+        if self.world == 1:
+            return None
+        torch, dist = self.torch, self.dist
+        if self.pack is not None:
+            self.pack(u, self.first_idx, 0, 0, self.send_first)
+            self.pack(u, self.last_idx, 0, 1, self.send_last)
+        else:
+            un = u.numpy() if hasattr(u, "numpy") else u
+            self.send_first.copy_(torch.from_numpy(pack_faces_host(un, self.part["send_first"], self.d, self.p1, 0, 0)))
+            self.send_last.copy_(torch.from_numpy(pack_faces_host(un, self.part["send_last"], self.d, self.p1, 0, 1)))
+        F = self.part["plane"]
+        nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        # tags disambiguate the two messages when both neighbours are one rank (W = 2)
+        ops = [
+            dist.P2POp(dist.isend, self.send_first, prv, group=self.group, tag=1),
+            dist.P2POp(dist.isend, self.send_last, nxt, group=self.group, tag=2),
+            dist.P2POp(dist.irecv, self.ghost[:F], nxt, group=self.group, tag=1),
+            dist.P2POp(dist.irecv, self.ghost[F:], prv, group=self.group, tag=2),
+        ]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return self.ghost

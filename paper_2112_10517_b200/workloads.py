@@ -1,0 +1,86 @@
+"""BASELINE.json configurations as concrete seeded inputs.
+
+The reference measures on its own ICs (no public dataset); these synthetic
+states stand in for BASELINE's five configs. Each builder returns
+``(setup, u, config)`` with ``u`` the conserved state (n_elem, nn, d+2)
+built with prim2cons (bit-identical to the reference's for the same inputs,
+tests/test_setup.py).
+
+  cfg1  2D N=3 16^2 Cartesian [-1,1]^2, Ranocha + Rusanov (llf), density wave
+  cfg2  3D N=3 16^3 Cartesian, Ranocha, density wave (volume integral)
+  cfg3  3D N=7 32^3 Cartesian, Chandrashekar, seeded random state
+  cfg4  3D N=4 48^3 curved (amplitude -0.1 in the reference's convention),
+        Kennedy-Gruber + llf, density wave, SSPRK43
+  cfg5  3D N=3 128^3 Cartesian, Ranocha / Shima + llf, perturbed wave with
+        the N(0,1) noise clipped to [-1, 1] (the literal state has rho <= 0
+        at 76,163 nodes)
+"""
+
+import numpy as np
+
+from .discretization import RhsConfig, build_setup
+from .euler import GasParams, prim2cons
+from .geometry import build_mesh
+from .operators import lgl_operator
+
+GAS = GasParams(1.4)
+
+CONFIGS = {
+    1: dict(dims=(16, 16), p=3, amplitude=0.0, volume_flux="ranocha", surface_flux="llf", state="wave"),
+    2: dict(dims=(16, 16, 16), p=3, amplitude=0.0, volume_flux="ranocha", surface_flux="llf", state="wave"),
+    3: dict(dims=(32, 32, 32), p=7, amplitude=0.0, volume_flux="chandrashekar", surface_flux="llf", state="random"),
+    4: dict(dims=(48, 48, 48), p=4, amplitude=-0.1, volume_flux="kennedy_gruber", surface_flux="llf", state="wave"),
+    5: dict(dims=(128, 128, 128), p=3, amplitude=0.0, volume_flux="ranocha", surface_flux="llf", state="noisy_wave"),
+}
+
+
+def wave_primitives(coords):
+    """rho = 1 + 0.98 sin(pi sum x), v = (0.1, 0.2[, 0.3]), p = 20."""
+    d = coords.shape[-1]
+    q = np.empty(coords.shape[:-1] + (d + 2,))
+    q[..., 0] = 1.0 + 0.98 * np.sin(np.pi * coords.sum(-1))
+    for i in range(d):
+        q[..., 1 + i] = (0.1, 0.2, 0.3)[i]
+    q[..., d + 1] = 20.0
+    return q
+
+
+def random_primitives(shape, d, seed=0):
+    """cfg3: rho = 1 + 0.1 U(-1,1); v_i ~ N(0, 0.1^2); p = 1 + 0.1 U(-1,1),
+    drawn from default_rng(seed) in this order over (n_elem, nn)."""
+    rng = np.random.default_rng(seed)
+    q = np.empty(shape + (d + 2,))
+    q[..., 0] = 1.0 + 0.1 * rng.uniform(-1.0, 1.0, size=shape)
+    for i in range(d):
+        q[..., 1 + i] = rng.normal(0.0, 0.1, size=shape)
+    q[..., d + 1] = 1.0 + 0.1 * rng.uniform(-1.0, 1.0, size=shape)
+    return q
+
+
+def noisy_wave_primitives(coords, seed=0):
+    """cfg5: the wave + 0.01 clip(N(0,1), -1, 1) on rho."""
+    q = wave_primitives(coords)
+    rng = np.random.default_rng(seed)
+    z = np.clip(rng.normal(size=coords.shape[:-1]), -1.0, 1.0)
+    q[..., 0] = q[..., 0] + 0.01 * z
+    return q
+
+
+def build(k, dims=None, kernel="batched", volume_flux=None, precompute=None):
+    """(setup, u, config) for BASELINE config ``k`` (optionally resized)."""
+    c = CONFIGS[k]
+    dims = tuple(dims) if dims is not None else c["dims"]
+    mesh = build_mesh(dims, bounds=(-1.0, 1.0), amplitude=c["amplitude"])
+    setup = build_setup(mesh, lgl_operator(c["p"]), GAS)
+    if c["state"] == "wave":
+        q = wave_primitives(setup.coords)
+    elif c["state"] == "random":
+        q = random_primitives((setup.n_elements, setup.n_nodes), setup.d)
+    else:
+        q = noisy_wave_primitives(setup.coords)
+    u = np.ascontiguousarray(prim2cons(q, GAS))
+    vf = volume_flux or c["volume_flux"]
+    if precompute is None:
+        precompute = "primitives_and_logs" if (kernel == "batched" and vf in ("ranocha", "chandrashekar")) else "none"
+    config = RhsConfig(volume_flux=vf, surface_flux=c["surface_flux"], precompute=precompute, kernel=kernel)
+    return setup, u, config

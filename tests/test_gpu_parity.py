@@ -1,0 +1,326 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference's golden outputs.
+
+Bars (written in each test):
+* kernel="reference" (FAITHFUL) is BITWISE equal to the oracle built with the
+  correctly rounded log (liboracle_cr.so), which is itself bitwise equal to
+  the reference except where glibc's log misrounds; against the reference's
+  own outputs du must agree to <= 1e-12 relative in max norm (literal
+  north-star bar).
+* kernel="batched" (FAST) volume integral: max|VOL - VOL_ref| <= 1e-12 max|VOL_ref|;
+  full RHS: max|du - du_ref| <= 1e-12 max(max|VOL_ref|, max|SURF_ref|)
+  (cancellation-aware bar).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2112_10517_b200 as P
+
+    return P
+
+
+def _rel(a, b, scale=None):
+    scale = np.abs(b).max() if scale is None else scale
+    return np.abs(a - b).max() / max(scale, 1e-300)
+
+
+# ---------------------------------------------------------------- FAITHFUL
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_faithful_volume_bitwise(name):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("vol_"):
+            continue
+        _, state, flux, pre = key.split("_", 3)
+        u = c["u_" + state]
+        got = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=flux, precompute=pre, kernel="reference"))
+        want = oracle.volume(u, setup, flux, pre, variant="cr")
+        assert np.array_equal(got, want), key
+        assert _rel(got, c[key]) <= 1e-13, key  # vs the reference's own bits
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_faithful_surface_bitwise(name):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("surf_"):
+            continue
+        _, state, flux = key.split("_", 2)
+        u = c["u_" + state]
+        got = P.surface_terms(u, setup, flux)
+        want = oracle.surface(u, setup, flux, variant="cr")
+        assert np.array_equal(got, want), key
+        if flux != "ranocha":  # no log in the other surface fluxes: reference bits
+            assert np.array_equal(got, c[key]), key
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_faithful_rhs_bitwise(name):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("rhs_"):
+            continue
+        parts = key.split("_")
+        state, vf, sf = parts[1], parts[2], parts[3]
+        pre = "primitives_and_logs" if key.endswith("_logs") else "none"
+        u = c["u_" + state]
+        got = P.rhs(u, setup, P.RhsConfig(volume_flux=vf, surface_flux=sf, precompute=pre, kernel="reference"))
+        assert np.array_equal(got, oracle.rhs(u, setup, vf, sf, pre, variant="cr")), key
+        assert _rel(got, c[key]) <= 1e-12, key  # literal du bar vs the reference
+
+
+@pytest.mark.parametrize("vf", ["kennedy_gruber", "chandrashekar"])
+@pytest.mark.parametrize("name", ["c2d_curv_p3", "c3d_cart_p3", "c3d_curv_p4"])
+def test_faithful_unpinned_fluxes_match_oracle(name, vf):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    u = c["u_rand"]
+    got = P.rhs(u, setup, P.RhsConfig(volume_flux=vf, surface_flux="llf", kernel="reference"))
+    assert np.array_equal(got, oracle.rhs(u, setup, vf, "llf", variant="cr"))
+
+
+def test_cfg1_faithful_bitwise_and_literal_du():
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    g = G.config(1)
+    setup, u, _ = workloads.build(1)
+    du = P.rhs(u, setup, P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="reference"))
+    assert np.array_equal(du, oracle.rhs(u, setup, "ranocha", "llf", variant="cr"))
+    assert _rel(du, g["du"]) <= 1e-12
+
+
+# -------------------------------------------------------------------- FAST
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_fast_volume_within_tolerance(name):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("vol_") or not key.endswith("_none"):
+            continue
+        _, state, flux, _ = key.split("_", 3)
+        u = c["u_" + state]
+        for pre in ("none", "primitives_and_logs"):
+            got = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=flux, precompute=pre, kernel="batched"))
+            assert _rel(got, c[key]) <= 1e-12, (key, pre)
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_fast_rhs_within_tolerance(name):
+    P = _pkg()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for key in c:
+        if not key.startswith("rhs_") or key.endswith("_logs"):
+            continue
+        parts = key.split("_")
+        state, vf, sf = parts[1], parts[2], parts[3]
+        u = c["u_" + state]
+        vol = c.get("vol_%s_%s_none" % (state, vf))
+        surf = c.get("surf_%s_%s" % (state, sf))
+        scale = max(np.abs(vol).max(), np.abs(surf).max())
+        for pre in ("none", "primitives_and_logs"):
+            got = P.rhs(u, setup, P.RhsConfig(volume_flux=vf, surface_flux=sf, precompute=pre, kernel="batched"))
+            assert _rel(got, c[key], scale) <= 1e-12, (key, pre)
+
+
+# ----------------------------------------------------------- full-size cfgs
+
+
+def test_cfg2_samples_and_checksum():
+    """BASELINE cfg2 (16^3, N=3, Ranocha) at full size: sampled elements
+    against the reference's scalar volume_fluxdiff, plus the whole-mesh
+    checksum of the reference's batched VOL."""
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    g = G.config(2)
+    setup, u, _ = workloads.build(2)
+    idx = g["elements"]
+    for kernel, pre, key, tol in (
+        ("reference", "none", "vol_ranocha", 1e-13),
+        ("reference", "primitives_and_logs", "vol_ranocha_logs", 1e-13),
+        ("batched", "primitives_and_logs", "vol_ranocha", 1e-12),
+        ("batched", "none", "vol_ranocha", 1e-12),
+    ):
+        vol = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="ranocha", precompute=pre, kernel=kernel))
+        assert _rel(vol[idx], g[key]) <= tol, (kernel, pre)
+        s = np.abs(vol).sum(axis=(0, 1))
+        assert np.all(np.abs(s - g["volb_ranocha_abs_sum"]) <= 1e-12 * g["volb_ranocha_abs_sum"]), (kernel, pre)
+
+
+def test_cfg4_samples_curved():
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    g = G.config(4)
+    setup, u, _ = workloads.build(4)
+    idx = g["elements"]
+    for flux in ("ranocha", "shima"):
+        ref = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=flux, kernel="reference"))
+        assert _rel(ref[idx], g["vol_" + flux]) <= 1e-13
+        fast = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=flux, kernel="batched"))
+        assert _rel(fast[idx], g["vol_" + flux]) <= 1e-12
+
+
+def test_cfg3_samples_n7():
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    g = G.config(3)
+    setup, u, _ = workloads.build(3)
+    idx = g["elements"]
+    ref = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="ranocha", kernel="reference"))
+    assert _rel(ref[idx], g["vol_ranocha"]) <= 1e-13
+    fast = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="ranocha", kernel="batched",
+                                                        precompute="primitives_and_logs"))
+    assert _rel(fast[idx], g["vol_ranocha"]) <= 1e-12
+    # Chandrashekar (cfg3's named flux, unpinned): FAST vs FAITHFUL on the full mesh
+    a = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="chandrashekar", kernel="reference"))
+    b = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="chandrashekar", kernel="batched",
+                                                     precompute="primitives_and_logs"))
+    assert _rel(b, a) <= 1e-12
+
+
+# ------------------------------------------------------------- properties
+
+
+@pytest.mark.parametrize("vf", ["ranocha", "shima", "kennedy_gruber", "chandrashekar", "central"])
+@pytest.mark.parametrize("kernel", ["reference", "batched"])
+def test_free_stream_on_curved_mesh(vf, kernel):
+    """A constant state stays constant on the warped mesh (metric identity)."""
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    setup, _, _ = workloads.build(4, dims=(6, 6, 6))
+    q = np.zeros((setup.n_elements, setup.n_nodes, 5))
+    q[..., 0] = 1.3
+    q[..., 1:4] = (0.1, -0.2, 0.3)
+    q[..., 4] = 2.0
+    u = P.prim2cons(q, setup.gas)
+    du = P.rhs(u, setup, P.RhsConfig(volume_flux=vf, surface_flux="llf", kernel=kernel))
+    assert np.abs(du).max() < 1e-11
+
+
+@pytest.mark.parametrize("kernel", ["reference", "batched"])
+def test_conservation_and_entropy_conservation(kernel):
+    P = _pkg()
+    setup = G.golden_setup("c3d_curv_p4")
+    from paper_2112_10517_b200 import workloads
+
+    setup, u, _ = workloads.build(4, dims=(4, 4, 4))
+    wbar = np.ones(1)
+    for _ in range(3):
+        wbar = np.kron(wbar, setup.op.weights)
+    du = P.rhs(u, setup, P.RhsConfig(volume_flux="ranocha", surface_flux="ranocha", kernel=kernel))
+    weights = wbar[None, :] * setup.metrics.jac
+    totals = np.sum(weights[..., None] * du, axis=(0, 1))
+    scale = np.sum(np.abs(weights[..., None] * du), axis=(0, 1))
+    assert np.all(np.abs(totals) <= 1e-12 * scale)
+    _, normalized = P.entropy_rate(u, du, setup)
+    assert abs(normalized) < 1e-12
+
+
+def test_counters_match_reference_contract():
+    P = _pkg()
+    c = G.case("c3d_curv_p2")
+    setup = G.golden_setup("c3d_curv_p2")
+    cnt = P.FluxCounter()
+    P.rhs(c["u_rand"], setup, P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="batched"), counter=cnt)
+    assert (cnt.two_point_evals, cnt.one_point_evals, cnt.logmean_evals) == tuple(c["counts_rand_ranocha_llf"])
+
+
+def test_gate_names_first_bad_node():
+    P = _pkg()
+    c = G.case("c2d_cart_p3")
+    setup = G.golden_setup("c2d_cart_p3")
+    u = c["u_rand"].copy()
+    u[1, 2, -1] = 0.01
+    u[4, 0, 0] = -1.0
+    with pytest.raises(P.AdmissibilityError, match="element 1, node 2"):
+        P.rhs(u, setup, P.RhsConfig(kernel="batched"))
+    with pytest.raises(P.AdmissibilityError, match="cons2prim"):
+        P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(kernel="batched"))
+
+
+# ------------------------------------------------------------ time stepping
+
+
+@pytest.mark.parametrize("name", ["c2d_cart_p3", "c3d_curv_p2", "c3d_curv_p4"])
+def test_device_rk54_faithful_bitwise(name):
+    import torch
+
+    P = _pkg()
+    from paper_2112_10517_b200.device import device_mesh_for
+
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    cfg = P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="reference")
+    dm = device_mesh_for(setup)
+    stepper = P.DeviceStepper(dm, cfg, P.RK54)
+    dt = float(c["rk54_dt"])
+    for state in G.states(name):
+        u = c["u_" + state]
+        got = stepper.step(torch.as_tensor(u, device="cuda"), dt).cpu().numpy()
+        want = oracle.rk54_step(u, dt, lambda v: oracle.rhs(v, setup, "ranocha", "llf", variant="cr"))
+        assert np.array_equal(got, want)
+        assert _rel(got, c["rk54_" + state]) <= 1e-14
+
+
+def test_device_ssprk43_faithful_bitwise():
+    import torch
+
+    P = _pkg()
+    from paper_2112_10517_b200.device import device_mesh_for
+
+    c = G.case("c3d_curv_p4")
+    setup = G.golden_setup("c3d_curv_p4")
+    cfg = P.RhsConfig(volume_flux="kennedy_gruber", surface_flux="llf", kernel="reference")
+    stepper = P.DeviceStepper(device_mesh_for(setup), cfg, P.SSPRK43)
+    u = c["u_wave"]
+    dt = 1e-3
+    got = stepper.step(torch.as_tensor(u, device="cuda"), dt).cpu().numpy()
+    want = oracle.ssprk43_step(u, dt, lambda v: oracle.rhs(v, setup, "kennedy_gruber", "llf", variant="cr"))
+    assert np.array_equal(got, want)
+
+
+def test_device_stepper_graph_and_divergence():
+    import torch
+
+    P = _pkg()
+    from paper_2112_10517_b200.device import device_mesh_for
+
+    c = G.case("c2d_cart_p3")
+    setup = G.golden_setup("c2d_cart_p3")
+    cfg = P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="batched")
+    st = P.DeviceStepper(device_mesh_for(setup), cfg, P.RK54)
+    u = torch.as_tensor(c["u_rand"], device="cuda")
+    plain = st.step(u, 1e-3).clone()
+    out = st.capture(u, 1e-3)
+    st.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, plain)
+    bad = u.clone()
+    bad[2, 3, 0] = -1.0
+    with pytest.raises(P.AdmissibilityError, match="element 2, node 3"):
+        st.step(bad, 1e-3)
