@@ -646,3 +646,6 @@ int or_node(const double *u, int d, double gamma, int flux, int pre, double *out
     out[6] = q.x1;
     return 0;
 }
+
+/* the log this build uses (glibc log, or log_cr with -DFDG_ORACLE_LOGCR) */
+double or_log(double x) { return OR_LOG(x); }

@@ -79,7 +79,18 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
     KParams& k = m->base;
     memset(&k, 0, sizeof(k));
-    for (int i = 0; i < m->p1 * m->p1; ++i) k.dsplit[i] = desc->dsplit[i];
+    for (int a = 0; a < m->p1; ++a)
+        for (int b = 0; b < m->p1; ++b)
+            if (a != b && desc->dsplit[a * m->p1 + b] == 0.0) {
+                delete m;
+                return fail(FDG_ERR_UNSUPPORTED, "split matrix has a zero off-diagonal entry (%d, %d)", a, b);
+            }
+    // per-direction pair weights: Dsplit[a,b] * Ja^n_n on Cartesian meshes
+    // (the reference's wi = cab * area, discretization.py:297-298), Dsplit on
+    // curved ones (discretization.py:318-320)
+    for (int n = 0; n < 3; ++n)
+        for (int i = 0; i < m->p1 * m->p1; ++i)
+            k.wts[n][i] = desc->cartesian ? desc->dsplit[i] * desc->areas[n] : desc->dsplit[i];
     k.w0 = desc->weights[0];
     k.wp = desc->weights[m->p1 - 1];
     for (int i = 0; i < 3; ++i) k.areas[i] = desc->areas[i];

@@ -75,6 +75,16 @@ __device__ __forceinline__ double rcp_nr1(double x)
     return fma(r, fma(-x, r, 1.0), r);
 }
 
+// ~1 ulp reciprocal without the IEEE-division slow path (FAST mode only)
+__device__ __forceinline__ double rcp_fast(double x)
+{
+    double r = rcp_approx(x);
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 template <int MODE>
 __device__ __forceinline__ double dlog(double x)
 {
@@ -140,31 +150,6 @@ __device__ __forceinline__ double inv_logmean_logs_f(double a, double b, double 
     return (lb - la) / (b - a);
 }
 
-// ----------------------------------------------------------- fast log means
-// The log mean of (a, b) is num/den with
-//   series (u < 1e-4):  num = a + b,      den = 2 + u(2/3 + u(2/5 + u 2/7))
-//   direct:             num = b - a,      den = log(b) - log(a)
-// and its reciprocal is den/num. Branch test without a division:
-//   u < eps  <=>  a(a-2b)+b^2 < eps (a(a+2b)+b^2)   (both > 0).
-// Both branches are evaluated and selected (no divergence).
-struct Frac {
-    double num, den;
-};
-
-__device__ __forceinline__ Frac logmean_frac(double a, double b, double la, double lb)
-{
-    double b2 = b * b;
-    double nu = fma(a, a - 2.0 * b, b2);
-    double de = fma(a, a + 2.0 * b, b2);
-    bool series = nu < SERIES_EPSILON * de;
-    double u = nu * rcp_nr1(de);
-    double poly = fma(u, fma(u, fma(u, 2.0 / 7.0, 2.0 / 5.0), 2.0 / 3.0), 2.0);
-    Frac r;
-    r.num = series ? a + b : b - a;
-    r.den = series ? poly : lb - la;
-    return r;
-}
-
 // ----------------------------------------------------------------- node data
 
 // Primitive (and staged extra) values of one node as the pair loop sees them.
@@ -187,7 +172,7 @@ __device__ __forceinline__ void cons2prim(const double* u, double& rho, double (
         if constexpr (D == 3) s = s + v[2] * v[2];
         p = gm1 * (u[D + 1] - 0.5 * rho * s);
     } else {
-        double ri = 1.0 / rho;
+        double ri = rcp_fast(rho);
         double s = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -210,11 +195,20 @@ __device__ __forceinline__ bool gate_ok(const double* u, double gm1)
     return (rho > 0.0) && (p > 0.0) && isfinite(rho) && isfinite(p);
 }
 
+}  // namespace fdg
+
+#include "fdg_fast.cuh"
+
+namespace fdg {
+
 // Stage one node: primitives + the extras the volume flux needs.
+// FAITHFUL: (rho, v, p) exactly as cons2prim computes them;
+// FAST: (rho, v/2, p/2) -- see fdg_fast.cuh.
 template <int D, int VF, int MODE, int LOGS>
 __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node(const double* u, double gm1)
 {
     constexpr int NX = n_extra(VF, LOGS);
+    if constexpr (MODE == FAST) return make_node_fast<D, VF, LOGS>(u, gm1);
     Node<D, NX> q;
     cons2prim<D, MODE>(u, q.rho, q.v, q.p, gm1);
     if constexpr (VF == F_RANOCHA && LOGS) {
@@ -306,34 +300,13 @@ __device__ __forceinline__ void flux_ranocha(const Node<D, NX>& l, const Node<D,
     double vn_l, vn_r;
     vn_pair<D, AXIS>(l.v, r.v, nrm, vn_l, vn_r);
     double rho_mean, inv_rho_p_mean;
-    if constexpr (MODE == FAITHFUL) {
-        if constexpr (LOGS) {
-            rho_mean = logmean_logs_f(l.rho, r.rho, l.x[0], r.x[0]);
-            inv_rho_p_mean = l.p * r.p *
-                inv_logmean_logs_f(l.rho * r.p, r.rho * l.p, l.x[0] + r.x[1], r.x[0] + l.x[1]);
-        } else {
-            rho_mean = logmean_f(l.rho, r.rho);
-            inv_rho_p_mean = l.p * r.p * inv_logmean_f(l.rho * r.p, r.rho * l.p);
-        }
+    if constexpr (LOGS) {
+        rho_mean = logmean_logs_f(l.rho, r.rho, l.x[0], r.x[0]);
+        inv_rho_p_mean = l.p * r.p *
+            inv_logmean_logs_f(l.rho * r.p, r.rho * l.p, l.x[0] + r.x[1], r.x[0] + l.x[1]);
     } else {
-        double a2 = l.rho * r.p, b2 = r.rho * l.p;
-        double la1, lb1, la2, lb2;
-        if constexpr (LOGS) {
-            la1 = l.x[0];
-            lb1 = r.x[0];
-            la2 = l.x[0] + r.x[1];
-            lb2 = r.x[0] + l.x[1];
-        } else {
-            la1 = 0.0;
-            lb1 = log(r.rho / l.rho);
-            la2 = 0.0;
-            lb2 = log(b2 / a2);
-        }
-        Frac m1 = logmean_frac(l.rho, r.rho, la1, lb1);  // <rho>_log = num1/den1
-        Frac m2 = logmean_frac(a2, b2, la2, lb2);        // 1/<rho p>_log = den2/num2
-        double rr = 1.0 / (m1.den * m2.num);
-        rho_mean = m1.num * m2.num * rr;
-        inv_rho_p_mean = l.p * r.p * (m2.den * m1.den * rr);
+        rho_mean = logmean_f(l.rho, r.rho);
+        inv_rho_p_mean = l.p * r.p * inv_logmean_f(l.rho * r.p, r.rho * l.p);
     }
     double p_avg = 0.5 * (l.p + r.p);
     double vn_avg = 0.5 * (vn_l + vn_r);
@@ -427,32 +400,9 @@ __device__ __forceinline__ void flux_chandrashekar(const Node<D, NX>& l, const N
     vn_pair<D, AXIS>(l.v, r.v, nrm, vn_l, vn_r);
     double rho_avg = 0.5 * (l.rho + r.rho);
     double beta_avg = 0.5 * (l.x[0] + r.x[0]);
-    double rho_mean, inv_beta_mean, p_tilde;
-    if constexpr (MODE == FAITHFUL) {
-        rho_mean = logmean_f(l.rho, r.rho);
-        inv_beta_mean = inv_logmean_f(l.x[0], r.x[0]);
-        p_tilde = rho_avg / (2.0 * beta_avg);
-    } else {
-        double la1, lb1, la2, lb2;
-        if constexpr (LOGS) {
-            la1 = l.x[1];
-            lb1 = r.x[1];
-            la2 = l.x[2];
-            lb2 = r.x[2];
-        } else {
-            la1 = 0.0;
-            lb1 = log(r.rho / l.rho);
-            la2 = 0.0;
-            lb2 = log(r.x[0] / l.x[0]);
-        }
-        Frac m1 = logmean_frac(l.rho, r.rho, la1, lb1);
-        Frac m2 = logmean_frac(l.x[0], r.x[0], la2, lb2);
-        double b2 = 2.0 * beta_avg;
-        double rr = 1.0 / (m1.den * m2.num * b2);
-        rho_mean = m1.num * (m2.num * b2) * rr;
-        inv_beta_mean = m2.den * (m1.den * b2) * rr;
-        p_tilde = rho_avg * (m1.den * m2.num) * rr;
-    }
+    const double rho_mean = logmean_f(l.rho, r.rho);
+    const double inv_beta_mean = inv_logmean_f(l.x[0], r.x[0]);
+    const double p_tilde = rho_avg / (2.0 * beta_avg);
     double vn_avg = 0.5 * (vn_l + vn_r);
     double f_rho = rho_mean * vn_avg;
     double v2_l = 0.0, v2_r = 0.0;
@@ -484,7 +434,8 @@ template <int D, int VF, int AXIS, int MODE, int LOGS, int NX>
 __device__ __forceinline__ void volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                             const Gas& gas, int pre, double* f)
 {
-    if constexpr (VF == F_SHIMA) flux_shima<D, AXIS, MODE>(l, r, nrm, gas.igm1, f);
+    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS>(l, r, nrm, gas.igm1, f);
+    else if constexpr (VF == F_SHIMA) flux_shima<D, AXIS, MODE>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_RANOCHA) flux_ranocha<D, AXIS, MODE, LOGS>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_CENTRAL) flux_central<D, AXIS, MODE>(l, r, nrm, gas.igm1, pre != PRE_NONE, f);
     else if constexpr (VF == F_KG) flux_kg<D, AXIS, MODE>(l, r, nrm, f);
@@ -571,6 +522,53 @@ __device__ __forceinline__ void flux_hll(const double* ul, const double* ur, con
     }
 }
 
+// FAST Rusanov flux: AXIS >= 0 is the Cartesian face (normal = area e_AXIS,
+// area = nrm[AXIS] > 0), AXIS < 0 a general scaled normal.
+template <int D, int AXIS>
+__device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur, const double* nrm, const Gas& gas,
+                                              double* f)
+{
+    const double ril = rcp_fast(ul[0]), rir = rcp_fast(ur[0]);
+    double vl[D], vr[D], kl = 0.0, kr = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        vl[i] = ul[1 + i] * ril;
+        vr[i] = ur[1 + i] * rir;
+        kl = fma(ul[1 + i], vl[i], kl);
+        kr = fma(ur[1 + i], vr[i], kr);
+    }
+    const double p_l = gas.gm1 * fma(-0.5, kl, ul[D + 1]);
+    const double p_r = gas.gm1 * fma(-0.5, kr, ur[D + 1]);
+    double norm, vns_l, vns_r;  // |n| and v.n with the scaled normal
+    if constexpr (AXIS >= 0) {
+        norm = nrm[AXIS];
+        vns_l = vl[AXIS] * norm;
+        vns_r = vr[AXIS] * norm;
+    } else {
+        double nn = 0.0;
+        vns_l = 0.0;
+        vns_r = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            nn = fma(nrm[i], nrm[i], nn);
+            vns_l = fma(vl[i], nrm[i], vns_l);
+            vns_r = fma(vr[i], nrm[i], vns_r);
+        }
+        norm = sqrt(nn);
+    }
+    const double inorm = rcp_fast(norm);
+    const double lam_l = fma(fabs(vns_l), inorm, sqrt(gas.gamma * p_l * ril));
+    const double lam_r = fma(fabs(vns_r), inorm, sqrt(gas.gamma * p_r * rir));
+    const double halfdiss = 0.5 * fmax(lam_l, lam_r) * norm;
+    f[0] = 0.5 * (ul[0] * vns_l + ur[0] * vns_r) - halfdiss * (ur[0] - ul[0]);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double pn = (AXIS >= 0) ? ((i == AXIS) ? (p_l + p_r) * norm : 0.0) : (p_l + p_r) * nrm[i];
+        f[1 + i] = 0.5 * (fma(ul[1 + i], vns_l, ur[1 + i] * vns_r) + pn) - halfdiss * (ur[1 + i] - ul[1 + i]);
+    }
+    f[D + 1] = 0.5 * fma(ul[D + 1] + p_l, vns_l, (ur[D + 1] + p_r) * vns_r) - halfdiss * (ur[D + 1] - ul[D + 1]);
+}
+
 // Two-point flux with conserved inputs for the interface (runtime kind).
 template <int D, int MODE>
 __device__ __noinline__ void surface_flux(int kind, const double* ul, const double* ur, const double* nrm,
@@ -585,36 +583,19 @@ __device__ __noinline__ void surface_flux(int kind, const double* ul, const doub
     // exactly as the conserved-input kernels do, no log tables
     // (surface_terms never passes precomputed data, discretization.py:742)
     switch (kind) {
-    case F_SHIMA: {
-        auto l = make_node<D, F_SHIMA, MODE, 0>(ul, gas.gm1);
-        auto r = make_node<D, F_SHIMA, MODE, 0>(ur, gas.gm1);
-        flux_shima<D, -1, MODE>(l, r, nrm, gas.igm1, f);
-        return;
+#define FDG_SURF_SYM(K)                                                 \
+    case K: {                                                           \
+        const auto l = make_node<D, K, MODE, 0>(ul, gas.gm1);           \
+        const auto r = make_node<D, K, MODE, 0>(ur, gas.gm1);           \
+        volume_flux<D, K, -1, MODE, 0>(l, r, nrm, gas, PRE_NONE, f);    \
+        return;                                                         \
     }
-    case F_RANOCHA: {
-        auto l = make_node<D, F_RANOCHA, MODE, 0>(ul, gas.gm1);
-        auto r = make_node<D, F_RANOCHA, MODE, 0>(ur, gas.gm1);
-        flux_ranocha<D, -1, MODE, 0>(l, r, nrm, gas.igm1, f);
-        return;
-    }
-    case F_CENTRAL: {
-        auto l = make_node<D, F_CENTRAL, MODE, 0>(ul, gas.gm1);
-        auto r = make_node<D, F_CENTRAL, MODE, 0>(ur, gas.gm1);
-        flux_central<D, -1, MODE>(l, r, nrm, gas.igm1, 0, f);
-        return;
-    }
-    case F_KG: {
-        auto l = make_node<D, F_KG, MODE, 0>(ul, gas.gm1);
-        auto r = make_node<D, F_KG, MODE, 0>(ur, gas.gm1);
-        flux_kg<D, -1, MODE>(l, r, nrm, f);
-        return;
-    }
-    case F_CHANDRASHEKAR: {
-        auto l = make_node<D, F_CHANDRASHEKAR, MODE, 0>(ul, gas.gm1);
-        auto r = make_node<D, F_CHANDRASHEKAR, MODE, 0>(ur, gas.gm1);
-        flux_chandrashekar<D, -1, MODE, 0>(l, r, nrm, gas.igm1, f);
-        return;
-    }
+        FDG_SURF_SYM(F_SHIMA)
+        FDG_SURF_SYM(F_RANOCHA)
+        FDG_SURF_SYM(F_CENTRAL)
+        FDG_SURF_SYM(F_KG)
+        FDG_SURF_SYM(F_CHANDRASHEKAR)
+#undef FDG_SURF_SYM
     default:
 #pragma unroll
         for (int v = 0; v < D + 2; ++v) f[v] = __longlong_as_double(0x7ff8000000000000ULL);

@@ -1,0 +1,236 @@
+// fdg_fast.cuh -- FAST-mode (RhsConfig.kernel == "batched") two-point fluxes.
+//
+// Same fluxes as the FAITHFUL ones in fdg_device.cuh, rearranged for the FP64
+// pipe of sm_100a:
+//   * nodes are staged with HALF velocities and HALF pressure (vh = v/2,
+//     ph = p/2; exact power-of-two scalings), so every arithmetic mean
+//     {a} = (a_l + a_r)/2 is a single add and the 1/2 factors of the fluxes
+//     fold away;
+//   * the log-mean branch test u < 1e-4 is d^2 < 1e-4 s^2 with d = b - a,
+//     s = b + a (no division); u itself (needed only in the series branch,
+//     where it is < 1e-4) uses an approximate reciprocal with one Newton step;
+//   * <x>_log = num/den with (num, den) = (s, P(u)) or (d, log b - log a); the
+//     two log means of a Ranocha pair share ONE reciprocal 1/(den_rho num_rhop)
+//     (MUFU.RCP64H + two Newton steps, branch free);
+//   * both branches are evaluated and selected (branch fractions mix inside
+//     every warp).
+// Results agree with the reference to a few ulps of each flux (VOL-level
+// relative differences ~1e-15, tests/test_gpu_parity.py).
+#pragma once
+
+namespace fdg {
+
+struct LogFrac {
+    double num, den;  // <a,b>_log = num / den
+};
+
+// log mean of (a, b) as a fraction; dl = log b - log a (only used off the series branch)
+__device__ __forceinline__ LogFrac logfrac(double a, double b, double dl)
+{
+    const double d = b - a;
+    const double s = b + a;
+    const bool series = d * d < SERIES_EPSILON * (s * s);
+    const double t = d * rcp_nr1(s);
+    const double u = t * t;
+    const double poly = fma(u, fma(u, fma(u, 2.0 / 7.0, 2.0 / 5.0), 2.0 / 3.0), 2.0);
+    LogFrac r;
+    r.num = series ? s : d;
+    r.den = series ? poly : dl;
+    return r;
+}
+
+// half-value dot products with the face/metric direction
+template <int D, int AXIS>
+__device__ __forceinline__ double hdot(const double (&vh)[D], const double* nrm)
+{
+    if constexpr (AXIS >= 0) {
+        return vh[AXIS];
+    } else {
+        double r = vh[0] * nrm[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) r = fma(vh[i], nrm[i], r);
+        return r;
+    }
+}
+
+// f_m_i = f_rho v_avg_i + p_avg n_i with v_avg = vh_l + vh_r, p_avg = ph_l + ph_r
+template <int D, int AXIS>
+__device__ __forceinline__ void fast_momentum(double f_rho, double p_avg, const double (&vhl)[D],
+                                              const double (&vhr)[D], const double* nrm, double* f)
+{
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double t = f_rho * (vhl[i] + vhr[i]);
+        if constexpr (AXIS >= 0) f[1 + i] = (i == AXIS) ? t + p_avg : t;
+        else f[1 + i] = fma(p_avg, nrm[i], t);
+    }
+}
+
+template <int D, int AXIS, int LOGS, int NX>
+__device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                             double igm1, double* f)
+{
+    // rho-mean and the (rho p)-mean; A = rho_l p_r / 2, B = rho_r p_l / 2
+    const double A = l.rho * r.p;
+    const double B = r.rho * l.p;
+    double dl1, dl2;
+    if constexpr (LOGS) {
+        dl1 = r.x[0] - l.x[0];
+        dl2 = (r.x[0] + l.x[1]) - (l.x[0] + r.x[1]);
+    } else {
+        dl1 = log(r.rho * rcp_fast(l.rho));
+        dl2 = log(B * rcp_fast(A));
+    }
+    const LogFrac m1 = logfrac(l.rho, r.rho, dl1);  // <rho>_log = num1/den1
+    const LogFrac m2 = logfrac(A, B, dl2);          // <rho p>_log = 2 num2/den2
+    const double rr = rcp_fast(m1.den * m2.num);
+    const double rho_mean = m1.num * m2.num * rr;
+    // igm1 p_l p_r / <rho p>_log = igm1 (4 ph_l ph_r) den2 / (2 num2)
+    const double e_int = (2.0 * igm1) * (l.p * r.p) * (m1.den * m2.den) * rr;
+    const double vn_l = hdot<D, AXIS>(l.v, nrm);
+    const double vn_r = hdot<D, AXIS>(r.v, nrm);
+    const double f_rho = rho_mean * (vn_l + vn_r);
+    double vv = l.v[0] * r.v[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
+    // f_E = f_rho (v_l.v_r / 2 + igm1 p_l p_r/<rho p>) + (p_l vn_r + p_r vn_l)/2
+    const double pv = fma(l.p, vn_r, r.p * vn_l);
+    f[0] = f_rho;
+    f[D + 1] = fma(f_rho, fma(2.0, vv, e_int), 2.0 * pv);
+    fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
+}
+
+template <int D, int AXIS, int NX>
+__device__ __forceinline__ void fast_shima(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                           double igm1, double* f)
+{
+    const double vn_l = hdot<D, AXIS>(l.v, nrm);
+    const double vn_r = hdot<D, AXIS>(r.v, nrm);
+    const double vn_avg = vn_l + vn_r;
+    const double p_avg = l.p + r.p;
+    const double f_rho = 0.5 * (l.rho + r.rho) * vn_avg;
+    double vv = l.v[0] * r.v[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
+    // f_E = f_rho v_l.v_r / 2 + p_avg vn_avg / (gamma-1) + (p_l vn_r + p_r vn_l)/2
+    const double pv = fma(l.p, vn_r, r.p * vn_l);
+    f[0] = f_rho;
+    f[D + 1] = fma(2.0 * f_rho, vv, fma(p_avg * vn_avg, igm1, 2.0 * pv));
+    fast_momentum<D, AXIS>(f_rho, p_avg, l.v, r.v, nrm, f);
+}
+
+// Kennedy-Gruber; x[0] holds e/2 (half specific total energy)
+template <int D, int AXIS, int NX>
+__device__ __forceinline__ void fast_kg(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm, double* f)
+{
+    const double vn_avg = hdot<D, AXIS>(l.v, nrm) + hdot<D, AXIS>(r.v, nrm);
+    const double p_avg = l.p + r.p;
+    const double f_rho = 0.5 * (l.rho + r.rho) * vn_avg;
+    f[0] = f_rho;
+    fast_momentum<D, AXIS>(f_rho, p_avg, l.v, r.v, nrm, f);
+    f[D + 1] = fma(f_rho, l.x[0] + r.x[0], p_avg * vn_avg);
+}
+
+// Chandrashekar; x[0] = beta = rho/(2p), x[1] = log rho, x[2] = log beta (LOGS)
+template <int D, int AXIS, int LOGS, int NX>
+__device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                                   double igm1, double* f)
+{
+    double dl1, dl2;
+    if constexpr (LOGS) {
+        dl1 = r.x[1] - l.x[1];
+        dl2 = r.x[2] - l.x[2];
+    } else {
+        dl1 = log(r.rho * rcp_fast(l.rho));
+        dl2 = log(r.x[0] * rcp_fast(l.x[0]));
+    }
+    const LogFrac m1 = logfrac(l.rho, r.rho, dl1);     // <rho>_log
+    const LogFrac m2 = logfrac(l.x[0], r.x[0], dl2);   // <beta>_log
+    const double bsum = l.x[0] + r.x[0];               // 2 {beta}
+    const double rr = rcp_fast(m1.den * m2.num * bsum);
+    const double rho_mean = m1.num * m2.num * bsum * rr;
+    const double inv_beta_mean = m2.den * m1.den * bsum * rr;
+    const double p_tilde = 0.5 * (l.rho + r.rho) * (m1.den * m2.num) * rr;  // {rho} / (2 {beta})
+    const double vn_avg = hdot<D, AXIS>(l.v, nrm) + hdot<D, AXIS>(r.v, nrm);
+    const double f_rho = rho_mean * vn_avg;
+    double v2 = 0.0;  // {|v|^2}/2 = |vh_l|^2 + |vh_r|^2
+#pragma unroll
+    for (int i = 0; i < D; ++i) v2 = fma(l.v[i], l.v[i], fma(r.v[i], r.v[i], v2));
+    f[0] = f_rho;
+    double work = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double va = l.v[i] + r.v[i];
+        const double t = f_rho * va;
+        if constexpr (AXIS >= 0) f[1 + i] = (i == AXIS) ? t + p_tilde : t;
+        else f[1 + i] = fma(p_tilde, nrm[i], t);
+        work = fma(va, f[1 + i], work);
+    }
+    f[D + 1] = fma(f_rho, fma(0.5 * igm1, inv_beta_mean, -v2), work);
+}
+
+// central (0.5 (f(u_l) + f(u_r)).n) from the staged conserved state x[0..D+1]
+template <int D, int AXIS, int NX>
+__device__ __forceinline__ void fast_central(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                             double* f)
+{
+    const double vn_l = hdot<D, AXIS>(l.v, nrm);  // half normal velocities
+    const double vn_r = hdot<D, AXIS>(r.v, nrm);
+    f[0] = l.x[0] * vn_l + r.x[0] * vn_r;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double t = fma(l.x[1 + i], vn_l, r.x[1 + i] * vn_r);
+        const double pn = l.p + r.p;  // half-pressure sum = {p}
+        if constexpr (AXIS >= 0) f[1 + i] = (i == AXIS) ? t + pn : t;
+        else f[1 + i] = fma(pn, nrm[i], t);
+    }
+    f[D + 1] = fma(l.x[D + 1] + 2.0 * l.p, vn_l, (r.x[D + 1] + 2.0 * r.p) * vn_r);
+}
+
+// FAST staging: rho, v/2, p/2 and the extras
+template <int D, int VF, int LOGS>
+__device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const double* u, double gm1)
+{
+    constexpr int NX = n_extra(VF, LOGS);
+    Node<D, NX> q;
+    const double rho = u[0];
+    const double hri = 0.5 * rcp_fast(rho);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        q.v[i] = u[1 + i] * hri;  // v/2
+        s = fma(q.v[i], q.v[i], s);
+    }
+    q.rho = rho;
+    // p/2 = (gamma-1)/2 (E - rho |v|^2 / 2) = (gamma-1)/2 (E - 2 rho |v/2|^2)
+    q.p = (0.5 * gm1) * fma(-2.0 * rho, s, u[D + 1]);
+    if constexpr (VF == F_RANOCHA && LOGS) {
+        q.x[0] = log(rho);
+        q.x[1] = log(2.0 * q.p);
+    } else if constexpr (VF == F_CHANDRASHEKAR) {
+        q.x[0] = 0.25 * rho * rcp_fast(q.p);  // beta = rho / (2 p)
+        if constexpr (LOGS) {
+            q.x[1] = log(rho);
+            q.x[2] = log(q.x[0]);
+        }
+    } else if constexpr (VF == F_KG) {
+        q.x[0] = u[D + 1] * hri;  // e/2
+    } else if constexpr (VF == F_CENTRAL) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) q.x[i] = (i < D + 2) ? u[i] : 0.0;
+    }
+    return q;
+}
+
+template <int D, int VF, int AXIS, int LOGS, int NX>
+__device__ __forceinline__ void fast_volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                                 double igm1, double* f)
+{
+    if constexpr (VF == F_SHIMA) fast_shima<D, AXIS>(l, r, nrm, igm1, f);
+    else if constexpr (VF == F_RANOCHA) fast_ranocha<D, AXIS, LOGS>(l, r, nrm, igm1, f);
+    else if constexpr (VF == F_CENTRAL) fast_central<D, AXIS>(l, r, nrm, f);
+    else if constexpr (VF == F_KG) fast_kg<D, AXIS>(l, r, nrm, f);
+    else fast_chandrashekar<D, AXIS, LOGS>(l, r, nrm, igm1, f);
+}
+
+}  // namespace fdg

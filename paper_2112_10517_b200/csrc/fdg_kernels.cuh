@@ -12,8 +12,8 @@
 //           evaluates each symmetric two-point flux ONCE, and scatters
 //           D[a,b] f into node a and D[b,a] f into node b in registers.  The
 //           per-node partial sums are carried across directions in shared
-//           memory, so every node sees the reference's accumulation order
-//           (discretization.py:288-320).
+//           memory (SoA, padded like the primitives), so every node sees the
+//           reference's accumulation order (discretization.py:288-320).
 //   epilogue VOL / J (mesh_fluxdiff_volume), or the LGL surface terms
 //           (both sides of each interface evaluated from identical
 //           arguments, lifted with 1/(w J), direction by direction,
@@ -23,6 +23,8 @@
 // HBM traffic per node for the volume integral: u read once (8 nvar B) and
 // VOL written once (8 nvar B) -- the algorithmic minimum.
 #pragma once
+#include <type_traits>
+
 #include "fdg_device.cuh"
 
 namespace fdg {
@@ -49,7 +51,7 @@ struct KParams {
     Status* status;
     long long n_elem;
     long long elem_base;      // added to element indices reported by the gate
-    double dsplit[64];        // (p+1)^2, build_dsplit(op).matrix (row-major)
+    double wts[3][64];        // per direction: Dsplit[a,b] * Ja^n_n (Cartesian) or Dsplit (curved)
     double areas[3];          // Cartesian Ja^n_n
     double jac_const;         // Cartesian J
     double w0, wp;            // LGL weights at the -1 / +1 ends
@@ -70,6 +72,8 @@ struct Geo {
     static constexpr int NNP = NN + NN / P1;  // one pad slot per innermost row
     static constexpr int EPB = LINES >= 128 ? 1 : 128 / LINES;
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
+    static constexpr int FS = EPB * NNP;      // stride of one primitive field
+    static constexpr int FA = EPB * NNP + 1;  // stride of one accumulator variable (odd: spreads banks)
 
     // node id of position a on line m of direction n (operators.py:248-259)
     template <int N>
@@ -79,13 +83,27 @@ struct Geo {
         return (m / stride * P1 + a) * stride + m % stride;
     }
     __device__ static __forceinline__ int pad(int node) { return node + node / P1; }
+    // accumulator slot of (variable v, element el, node)
+    __device__ static __forceinline__ int acc(int v, int el, int node) { return v * FA + el * NNP + pad(node); }
 };
 
 template <int D, int P1, int VF, int LOGS>
 __host__ __device__ constexpr int smem_doubles()
 {
     using G = Geo<D, P1>;
-    return (2 + D + n_extra(VF, LOGS)) * G::EPB * G::NNP + G::EPB * G::NN * G::NVAR;
+    // primitive fields + accumulators (the accumulator block doubles as the
+    // AoS staging buffer of u, which is smaller)
+    return (2 + D + n_extra(VF, LOGS)) * G::FS + G::NVAR * G::FA;
+}
+
+// compile-time for loop: f(integral_constant<int, i>) for i in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void sfor(F&& f)
+{
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        sfor<B + 1, E>(f);
+    }
 }
 
 template <int D, int NX>
@@ -121,7 +139,6 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
     constexpr int NX = n_extra(VF, LOGS);
-    constexpr int FS = G::EPB * G::NNP;
     double acc[P1][NVAR];
     int nodes[P1];
 #pragma unroll
@@ -135,7 +152,7 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
 #pragma unroll
         for (int a = 0; a < P1; ++a)
 #pragma unroll
-            for (int v = 0; v < NVAR; ++v) acc[a][v] = sacc[(el * G::NN + nodes[a]) * NVAR + v];
+            for (int v = 0; v < NVAR; ++v) acc[a][v] = sacc[G::acc(v, el, nodes[a])];
     }
     double jl[CURVED ? P1 : 1][D];
     if constexpr (CURVED) {
@@ -145,40 +162,37 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
             for (int j = 0; j < D; ++j) jl[a][j] = __ldg(prm.ja + ((e * G::NN + nodes[a]) * D + N) * D + j);
     }
     const int sbase = el * G::NNP;
-#pragma unroll
-    for (int a = 0; a < P1; ++a) {
-        const Node<D, NX> qa = load_node<D, NX>(sq, FS, sbase + G::pad(nodes[a]));
-#pragma unroll
-        for (int b = a + 1; b < P1; ++b) {
-            const double cab = prm.dsplit[a * P1 + b];
-            const double cba = prm.dsplit[b * P1 + a];
-            if (cab == 0.0 && cba == 0.0) continue;  // pair_table drops all-zero pairs
-            const Node<D, NX> qb = load_node<D, NX>(sq, FS, sbase + G::pad(nodes[b]));
+    // compile-time pair loops (a < b in pair-table order): keeps acc/jl in registers
+    sfor<0, P1>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        const Node<D, NX> qa = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[a]));
+        sfor<a + 1, P1>([&](auto B) {
+            constexpr int b = decltype(B)::value;
+            // every off-diagonal LGL Dsplit entry is nonzero (checked at mesh
+            // creation), so the reference's pair table visits every pair
+            const double wa = prm.wts[N][a * P1 + b];
+            const double wb = prm.wts[N][b * P1 + a];
+            const Node<D, NX> qb = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[b]));
             double f[NVAR];
-            double wa, wb;
             if constexpr (CURVED) {
                 double alpha[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) alpha[j] = 0.5 * (jl[a][j] + jl[b][j]);
                 volume_flux<D, VF, -1, MODE, LOGS>(qa, qb, alpha, prm.gas, prm.precompute, f);
-                wa = cab;
-                wb = cba;
             } else {
                 volume_flux<D, VF, N, MODE, LOGS>(qa, qb, nullptr, prm.gas, prm.precompute, f);
-                wa = cab * prm.areas[N];
-                wb = cba * prm.areas[N];
             }
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) {
                 acc[a][v] += wa * f[v];
                 acc[b][v] += wb * f[v];
             }
-        }
-    }
+        });
+    });
 #pragma unroll
     for (int a = 0; a < P1; ++a)
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) sacc[(el * G::NN + nodes[a]) * NVAR + v] = acc[a][v];
+        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, nodes[a])] = acc[a][v];
 }
 
 template <int D>
@@ -186,6 +200,20 @@ __device__ __forceinline__ void load_state(const double* src, double* s)
 {
 #pragma unroll
     for (int v = 0; v < D + 2; ++v) s[v] = __ldg(src + v);
+}
+
+// Interface flux: Rusanov inline (the common case, registers only), the other
+// kinds through the out-of-line dispatcher.
+template <int D, bool CURVED, int MODE, int N>
+__device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, const double* ur, const double* nrm,
+                                          double* f)
+{
+    if (prm.surface_flux == F_LLF) {
+        if constexpr (MODE == FAST) flux_llf_fast<D, CURVED ? -1 : N>(ul, ur, nrm, prm.gas, f);
+        else flux_llf<D, MODE>(ul, ur, nrm, prm.gas, f);
+    } else {
+        surface_flux<D, MODE>(prm.surface_flux, ul, ur, nrm, prm.gas, f);
+    }
 }
 
 // Interface terms of direction N for the thread's line (both of its ends).
@@ -210,12 +238,11 @@ __device__ __forceinline__ void surface_direction(const KParams& prm, double* sa
 #pragma unroll
             for (int j = 0; j < D; ++j) nrm[j] = (j == N) ? prm.areas[N] : 0.0;
         }
-        surface_flux<D, MODE>(prm.surface_flux, ul, ur, nrm, prm.gas, f);
+        face_flux<D, CURVED, MODE, N>(prm, ul, ur, nrm, f);
         const double J = CURVED ? __ldg(prm.jac + e * G::NN + im) : prm.jac_const;
         const double sm = 1.0 / (prm.wp * J);
-        double* o = sacc + (el * G::NN + im) * NVAR;
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) o[v] += sm * f[v];
+        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, im)] += sm * f[v];
     }
     // -N face of e (e is the plus element): neighbour's line end, own line start
     {
@@ -241,12 +268,11 @@ __device__ __forceinline__ void surface_direction(const KParams& prm, double* sa
             for (int j = 0; j < D; ++j) nrm[j] = (j == N) ? prm.areas[N] : 0.0;
         }
         load_state<D>(prm.u + (e * G::NN + ip) * NVAR, ur);
-        surface_flux<D, MODE>(prm.surface_flux, ul, ur, nrm, prm.gas, f);
+        face_flux<D, CURVED, MODE, N>(prm, ul, ur, nrm, f);
         const double J = CURVED ? __ldg(prm.jac + e * G::NN + ip) : prm.jac_const;
         const double sp = 1.0 / (prm.w0 * J);
-        double* o = sacc + (el * G::NN + ip) * NVAR;
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) o[v] -= sp * f[v];
+        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, ip)] -= sp * f[v];
     }
 }
 
@@ -256,10 +282,9 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
     using G = Geo<D, P1>;
     constexpr int NN = G::NN, NVAR = G::NVAR, EPB = G::EPB, NT = G::NT;
     constexpr int NX = n_extra(VF, LOGS);
-    constexpr int FS = EPB * G::NNP;
     extern __shared__ double smem[];
-    double* sq = smem;                           // (2+D+NX) fields x EPB x NNP
-    double* sacc = smem + (2 + D + NX) * FS;     // EPB x NN x NVAR
+    double* sq = smem;                        // (2+D+NX) fields x FS
+    double* sacc = smem + (2 + D + NX) * G::FS;  // NVAR x FA (AoS u staging before the volume pass)
     const int tid = threadIdx.x;
     const int el = tid / G::LINES;
     const int m = tid % G::LINES;
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
         const bool active = (el < ne);
 
         if (epi != EPI_SURFACE) {
-            // ---- stage: coalesced copy, then primitives per node
+            // ---- stage: coalesced copy (AoS), then primitives per node (SoA)
             for (int t = tid; t < count; t += NT) sacc[t] = __ldg(prm.u + base + t);
             __syncthreads();
             for (int t = tid; t < ne * NN; t += NT) {
@@ -284,10 +309,10 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
                 if (!gate_ok<D>(su, prm.gas.gm1))
                     atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN + t));
                 const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
-                store_node<D, NX>(sq, FS, tel * G::NNP + G::pad(node), q);
+                store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
             }
             __syncthreads();
-            // ---- volume integral, direction by direction
+            // ---- volume integral, direction by direction (accumulators: SoA)
             if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e);
             __syncthreads();
             if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e);
@@ -298,12 +323,14 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
             }
             // ---- VOL = acc / J
             for (int t = tid; t < count; t += NT) {
-                const int node = (t / NVAR) % NN;
-                const double J = CURVED ? __ldg(prm.jac + e0 * NN + t / NVAR) : prm.jac_const;
-                const double vol = sacc[t] / J;
+                const int tel = t / (NN * NVAR);
+                const int r = t - tel * NN * NVAR;
+                const int node = r / NVAR, v = r - node * NVAR;
+                const double J = CURVED ? __ldg(prm.jac + (e0 + tel) * NN + node) : prm.jac_const;
+                const int s = G::acc(v, tel, node);
+                const double vol = sacc[s] / J;
                 if (epi == EPI_VOLUME) prm.out[base + t] = vol;
-                else sacc[t] = vol;
-                (void)node;
+                else sacc[s] = vol;
             }
             if (epi == EPI_VOLUME) {
                 __syncthreads();
@@ -311,7 +338,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
             }
         } else {
             // mesh_surface: accumulate into the caller's array
-            for (int t = tid; t < count; t += NT) sacc[t] = prm.out[base + t];
+            for (int t = tid; t < count; t += NT) {
+                const int tel = t / (NN * NVAR);
+                const int r = t - tel * NN * NVAR;
+                const int node = r / NVAR, v = r - node * NVAR;
+                sacc[G::acc(v, tel, node)] = prm.out[base + t];
+            }
         }
         __syncthreads();
         // ---- interface terms, direction by direction
@@ -324,35 +356,39 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
             __syncthreads();
         }
         // ---- outputs
-        if (epi == EPI_SURFACE) {
-            for (int t = tid; t < count; t += NT) prm.out[base + t] = sacc[t];
-        } else if (epi == EPI_RHS) {
-            for (int t = tid; t < count; t += NT) prm.out[base + t] = -sacc[t];
-        } else {  // EPI_STAGE
-            bool bad = false;
-            for (int t = tid; t < count; t += NT) {
-                const double k = -sacc[t];
+        bool bad = false;
+        for (int t = tid; t < count; t += NT) {
+            const int tel = t / (NN * NVAR);
+            const int r = t - tel * NN * NVAR;
+            const int node = r / NVAR, v = r - node * NVAR;
+            const double val = sacc[G::acc(v, tel, node)];
+            if (epi == EPI_SURFACE) {
+                prm.out[base + t] = val;
+            } else if (epi == EPI_RHS) {
+                prm.out[base + t] = -val;
+            } else {  // EPI_STAGE
+                const double k = -val;
                 const double x = __ldg(prm.u + base + t);
                 double y;
                 if (prm.stage_kind == 0) {
                     // du = a_i du + dt k ; v = v + b_i du     (timeint.py:157-158)
                     // (a_0 == 0: the register starts at zero, nothing to read)
-                    double r;
-                    if (prm.sa == 0.0) r = prm.dt * k;
-                    else if constexpr (MODE == FAST) r = fma(prm.sa, prm.reg[base + t], prm.dt * k);
-                    else r = prm.sa * prm.reg[base + t] + prm.dt * k;
-                    prm.reg[base + t] = r;
-                    y = x + prm.sb * r;
+                    double rg;
+                    if (prm.sa == 0.0) rg = prm.dt * k;
+                    else if constexpr (MODE == FAST) rg = fma(prm.sa, prm.reg[base + t], prm.dt * k);
+                    else rg = prm.sa * prm.reg[base + t] + prm.dt * k;
+                    prm.reg[base + t] = rg;
+                    y = x + prm.sb * rg;
                 } else {
                     // y = (A u0 + B x) + (C dt) k             (Shu-Osher SSPRK43)
-                    double s = (prm.sa != 0.0) ? prm.sa * __ldg(prm.u0 + base + t) + prm.sb * x : x;
+                    const double s = (prm.sa != 0.0) ? prm.sa * __ldg(prm.u0 + base + t) + prm.sb * x : x;
                     y = s + prm.sc * k;
                 }
                 prm.out[base + t] = y;
                 bad |= !isfinite(y);
             }
-            if (bad) atomicMin(&prm.status->bad_stage, prm.stage_index);
         }
+        if (bad) atomicMin(&prm.status->bad_stage, prm.stage_index);
         __syncthreads();
     }
 }
