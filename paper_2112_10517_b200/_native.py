@@ -10,7 +10,7 @@ import os
 from .errors import ConfigurationError, NativeLibraryError, UnsupportedOperatorError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfdg.so")
+LIB_PATH = os.environ.get("FDG_LIB") or os.path.join(HERE, "libfdg.so")  # FDG_LIB: tuning variants only
 
 FLUX_IDS = {
     "central": 0,

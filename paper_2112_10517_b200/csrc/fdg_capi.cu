@@ -95,6 +95,7 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     k.wp = desc->weights[m->p1 - 1];
     for (int i = 0; i < 3; ++i) k.areas[i] = desc->areas[i];
     k.jac_const = desc->jac_const;
+    k.rjac_const = desc->cartesian ? 1.0 / desc->jac_const : 0.0;
     k.ja = desc->ja;
     k.jac = desc->jac;
     k.plus = desc->plus;

@@ -195,6 +195,19 @@ __device__ __forceinline__ bool gate_ok(const double* u, double gm1)
     return (rho > 0.0) && (p > 0.0) && isfinite(rho) && isfinite(p);
 }
 
+// Same decision without the division in the common case: the FMA-path
+// pressure p_fast and the gate's pressure differ by a few ulps of
+// (gamma-1) max(|E|, kinetic); whenever |p_fast| exceeds 1e-10 (gamma-1)|E|
+// their signs agree, otherwise the gate's own formula decides.
+template <int D>
+__device__ __forceinline__ bool gate_ok_fast(const double* u, double p_fast, double gm1)
+{
+    const double rho = u[0];
+    if ((rho > 0.0) && isfinite(rho) && isfinite(p_fast) && fabs(p_fast) > 1e-10 * gm1 * fabs(u[D + 1]))
+        return p_fast > 0.0;
+    return gate_ok<D>(u, gm1);
+}
+
 }  // namespace fdg
 
 #include "fdg_fast.cuh"

@@ -100,6 +100,55 @@ __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D,
     fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
 }
 
+// W independent Ranocha pairs evaluated statement by statement side by side:
+// the FP64 pipe needs ~4 independent instructions in flight per scheduler
+// (DFMA latency 8.3 cycles, one warp-DFMA issued per 2 cycles, measured by
+// scripts/micro/fp64_latency.cu); one pair's dependency chain is ~25 deep,
+// so interleaving W pairs multiplies the available ILP by W.
+template <int D, int AXIS, int LOGS, int NX, int W>
+__device__ __forceinline__ void fast_ranocha_w(const Node<D, NX>* const (&L)[W], const Node<D, NX>* const (&R)[W],
+                                               const double (&nrm)[W][D], double igm1, double (&f)[W][D + 2])
+{
+    double A[W], B[W], dl1[W], dl2[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        A[w] = L[w]->rho * R[w]->p;
+        B[w] = R[w]->rho * L[w]->p;
+        if constexpr (LOGS) {
+            dl1[w] = R[w]->x[0] - L[w]->x[0];
+            dl2[w] = (R[w]->x[0] + L[w]->x[1]) - (L[w]->x[0] + R[w]->x[1]);
+        } else {
+            dl1[w] = log(R[w]->rho * rcp_fast(L[w]->rho));
+            dl2[w] = log(B[w] * rcp_fast(A[w]));
+        }
+    }
+    LogFrac m1[W], m2[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) m1[w] = logfrac(L[w]->rho, R[w]->rho, dl1[w]);
+#pragma unroll
+    for (int w = 0; w < W; ++w) m2[w] = logfrac(A[w], B[w], dl2[w]);
+    double rr[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) rr[w] = rcp_fast(m1[w].den * m2[w].num);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const Node<D, NX>& l = *L[w];
+        const Node<D, NX>& r = *R[w];
+        const double rho_mean = m1[w].num * m2[w].num * rr[w];
+        const double e_int = (2.0 * igm1) * (l.p * r.p) * (m1[w].den * m2[w].den) * rr[w];
+        const double vn_l = hdot<D, AXIS>(l.v, nrm[w]);
+        const double vn_r = hdot<D, AXIS>(r.v, nrm[w]);
+        const double f_rho = rho_mean * (vn_l + vn_r);
+        double vv = l.v[0] * r.v[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
+        const double pv = fma(l.p, vn_r, r.p * vn_l);
+        f[w][0] = f_rho;
+        f[w][D + 1] = fma(f_rho, fma(2.0, vv, e_int), 2.0 * pv);
+        fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm[w], f[w]);
+    }
+}
+
 template <int D, int AXIS, int NX>
 __device__ __forceinline__ void fast_shima(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                            double igm1, double* f)

@@ -54,6 +54,7 @@ struct KParams {
     double wts[3][64];        // per direction: Dsplit[a,b] * Ja^n_n (Cartesian) or Dsplit (curved)
     double areas[3];          // Cartesian Ja^n_n
     double jac_const;         // Cartesian J
+    double rjac_const;        // 1/J (FAST)
     double w0, wp;            // LGL weights at the -1 / +1 ends
     Gas gas;
     int epilogue;
@@ -64,16 +65,45 @@ struct KParams {
     double sa, sb, sc, dt;    // 2N: a_i, b_i, -, dt ; SO: A, B, C*dt, -
 };
 
+// tuning knobs (compile-time; scripts/variants.sh builds alternatives)
+// Defaults measured on B200 (scripts/variants.sh + scripts/sweep.py):
+// 64-thread CTAs and a register cap that keeps 6 CTAs resident for p <= 4
+// (cfg2 16^3: 10.7 -> 12.8 G nodes/s, 64^3: 21.9 -> 22.5).
+#ifndef FDG_TARGET_THREADS
+#define FDG_TARGET_THREADS 64
+#endif
+#ifndef FDG_MIN_BLOCKS
+#define FDG_MIN_BLOCKS 0  // 0: per-degree default below
+#endif
+#ifndef FDG_LINE_REGS
+#define FDG_LINE_REGS 0
+#endif
+#ifndef FDG_STAGE_UNROLL
+#define FDG_STAGE_UNROLL 2
+#endif
+constexpr int kStageUnroll = FDG_STAGE_UNROLL;
+#ifndef FDG_PAD
+#define FDG_PAD 1
+#endif
+#ifndef FDG_PREFETCH
+#define FDG_PREFETCH 1
+#endif
+
 template <int D, int P1>
 struct Geo {
     static constexpr int NN = ipow(P1, D);
     static constexpr int LINES = ipow(P1, D - 1);
     static constexpr int NVAR = D + 2;
-    static constexpr int NNP = NN + NN / P1;  // one pad slot per innermost row
-    static constexpr int EPB = LINES >= 128 ? 1 : 128 / LINES;
+    static constexpr int NNP = NN + FDG_PAD * (NN / P1);  // one pad slot per innermost row
+    static constexpr int EPB = LINES >= FDG_TARGET_THREADS ? 1 : FDG_TARGET_THREADS / LINES;
+    // resident-CTA hint for __launch_bounds__ (register cap 64K / (NT * MINB))
+    static constexpr int MINB = FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (P1 <= 5 ? 6 : 1);
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
     static constexpr int FS = EPB * NNP;      // stride of one primitive field
     static constexpr int FA = EPB * NNP + 1;  // stride of one accumulator variable (odd: spreads banks)
+    static constexpr int NF = 2 * D * LINES;  // face nodes per element (2 sides x d directions)
+
+    __host__ __device__ static constexpr int stride(int n) { return ipow(P1, D - 1 - n); }
 
     // node id of position a on line m of direction n (operators.py:248-259)
     template <int N>
@@ -82,18 +112,27 @@ struct Geo {
         constexpr int stride = ipow(P1, D - 1 - N);
         return (m / stride * P1 + a) * stride + m % stride;
     }
-    __device__ static __forceinline__ int pad(int node) { return node + node / P1; }
+    __device__ static __forceinline__ int pad(int node) { return FDG_PAD ? node + node / P1 : node; }
     // accumulator slot of (variable v, element el, node)
     __device__ static __forceinline__ int acc(int v, int el, int node) { return v * FA + el * NNP + pad(node); }
 };
 
 template <int D, int P1, int VF, int LOGS>
+__host__ __device__ constexpr int sq_doubles()
+{
+    using G = Geo<D, P1>;
+    constexpr int prims = (2 + D + n_extra(VF, LOGS)) * G::FS;
+    constexpr int faces = G::EPB * G::NF * G::NVAR;
+    return prims > faces ? prims : faces;
+}
+
+template <int D, int P1, int VF, int LOGS>
 __host__ __device__ constexpr int smem_doubles()
 {
     using G = Geo<D, P1>;
-    // primitive fields + accumulators (the accumulator block doubles as the
-    // AoS staging buffer of u, which is smaller)
-    return (2 + D + n_extra(VF, LOGS)) * G::FS + G::NVAR * G::FA;
+    // primitive fields (later: the face-flux buffer) + accumulators (the
+    // accumulator block doubles as the AoS staging buffer of u, which is smaller)
+    return sq_doubles<D, P1, VF, LOGS>() + G::NVAR * G::FA;
 }
 
 // compile-time for loop: f(integral_constant<int, i>) for i in [B, E)
@@ -131,6 +170,77 @@ __device__ __forceinline__ Node<D, NX> load_node(const double* sq, int fs, int i
     return q;
 }
 
+// Round-robin (circle method) order of the p(p+1)/2 pairs of a line: every
+// round is a set of disjoint pairs, so consecutive pairs update different
+// accumulators (FAST mode; FAITHFUL keeps the pair-table order).
+template <int P1>
+struct Tour {
+    static constexpr int NP = P1 * (P1 - 1) / 2;
+    int a[NP > 0 ? NP : 1], b[NP > 0 ? NP : 1];
+};
+
+template <int P1>
+__host__ __device__ constexpr Tour<P1> tournament()
+{
+    Tour<P1> t{};
+    const int n = P1 + (P1 % 2);  // even number of slots (one dummy if P1 is odd)
+    int k = 0;
+    for (int r = 0; r < n - 1; ++r) {
+        for (int i = 0; i < n / 2; ++i) {
+            int x = (i == 0) ? n - 1 : (r + i) % (n - 1);
+            int y = (i == 0) ? r : (r - i + (n - 1)) % (n - 1);
+            if (x >= P1 || y >= P1) continue;  // the dummy's pairing: a bye
+            t.a[k] = x < y ? x : y;
+            t.b[k] = x < y ? y : x;
+            ++k;
+        }
+    }
+    return t;
+}
+
+#ifndef FDG_WIDE
+#define FDG_WIDE 1  // measured: no gain over the compiler's own interleaving (W = 2, 3, 6)
+#endif
+
+// FAST Ranocha, W pairs side by side in round-robin order (line data in registers)
+template <int D, int P1, bool CURVED, int LOGS, int N, int NX>
+__device__ __forceinline__ void volume_pairs_wide(const KParams& prm, const Node<D, NX> (&q)[P1],
+                                                  const double (&jl)[CURVED ? P1 : 1][D],
+                                                  double (&acc)[P1][D + 2])
+{
+    constexpr Tour<P1> T = tournament<P1>();
+    constexpr int NP = Tour<P1>::NP;
+    constexpr int W = FDG_WIDE;
+    sfor<0, (NP + W - 1) / W>([&](auto C) {
+        constexpr int k0 = decltype(C)::value * W;
+        constexpr int WE = (NP - k0) < W ? (NP - k0) : W;
+        const Node<D, NX>* L[WE];
+        const Node<D, NX>* R[WE];
+        double nrm[WE][D];
+        double f[WE][D + 2];
+        sfor<0, WE>([&](auto I) {
+            constexpr int w = decltype(I)::value;
+            constexpr int a = T.a[k0 + w], b = T.b[k0 + w];
+            L[w] = &q[a];
+            R[w] = &q[b];
+#pragma unroll
+            for (int j = 0; j < D; ++j) nrm[w][j] = CURVED ? 0.5 * (jl[CURVED ? a : 0][j] + jl[CURVED ? b : 0][j]) : 0.0;
+        });
+        fast_ranocha_w<D, CURVED ? -1 : N, LOGS, NX, WE>(L, R, nrm, prm.gas.igm1, f);
+        sfor<0, WE>([&](auto I) {
+            constexpr int w = decltype(I)::value;
+            constexpr int a = T.a[k0 + w], b = T.b[k0 + w];
+            const double wa = prm.wts[N][a * P1 + b];
+            const double wb = prm.wts[N][b * P1 + a];
+#pragma unroll
+            for (int v = 0; v < D + 2; ++v) {
+                acc[a][v] = fma(wa, f[w][v], acc[a][v]);
+                acc[b][v] = fma(wb, f[w][v], acc[b][v]);
+            }
+        });
+    });
+}
+
 // One direction of the volume integral for the thread's line.
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
 __device__ __forceinline__ void volume_direction(const KParams& prm, const double* sq, double* sacc, int el,
@@ -162,17 +272,47 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
             for (int j = 0; j < D; ++j) jl[a][j] = __ldg(prm.ja + ((e * G::NN + nodes[a]) * D + N) * D + j);
     }
     const int sbase = el * G::NNP;
+    if constexpr (MODE == FAST && VF == F_RANOCHA && FDG_WIDE > 1) {
+        Node<D, NX> ql[P1];
+        sfor<0, P1>([&](auto A) {
+            constexpr int a = decltype(A)::value;
+            ql[a] = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[a]));
+        });
+        volume_pairs_wide<D, P1, CURVED, LOGS, N>(prm, ql, jl, acc);
+#pragma unroll
+        for (int a = 0; a < P1; ++a)
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, nodes[a])] = acc[a][v];
+        return;
+    }
+#if FDG_LINE_REGS
+    // the whole line's node data in registers: P1 shared-memory loads per node
+    // instead of one per pair it takes part in
+    Node<D, NX> qline[P1];
+    sfor<0, P1>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        qline[a] = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[a]));
+    });
+#endif
     // compile-time pair loops (a < b in pair-table order): keeps acc/jl in registers
     sfor<0, P1>([&](auto A) {
         constexpr int a = decltype(A)::value;
+#if FDG_LINE_REGS
+        const Node<D, NX>& qa = qline[a];
+#else
         const Node<D, NX> qa = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[a]));
+#endif
         sfor<a + 1, P1>([&](auto B) {
             constexpr int b = decltype(B)::value;
             // every off-diagonal LGL Dsplit entry is nonzero (checked at mesh
             // creation), so the reference's pair table visits every pair
             const double wa = prm.wts[N][a * P1 + b];
             const double wb = prm.wts[N][b * P1 + a];
+#if FDG_LINE_REGS
+            const Node<D, NX>& qb = qline[b];
+#else
             const Node<D, NX> qb = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[b]));
+#endif
             double f[NVAR];
             if constexpr (CURVED) {
                 double alpha[D];
@@ -216,44 +356,38 @@ __device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, 
     }
 }
 
-// Interface terms of direction N for the thread's line (both of its ends).
-template <int D, int P1, bool CURVED, int MODE, int N>
-__device__ __forceinline__ void surface_direction(const KParams& prm, double* sacc, int el, int m, long long e)
+// Interface flux of one face node of element e: direction n, side 1 = its
+// +n face (e is the minus element), side 0 = its -n face (e is the plus
+// element); line m of direction n. Same arguments from both adjacent
+// elements, so both see identical bits (discretization.py:730-760 evaluates
+// each face once and scatters both ways).
+template <int D, int P1, bool CURVED, int MODE>
+__device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, int n, int side, int m, double* f)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
     constexpr int FN = G::LINES;
-    double ul[NVAR], ur[NVAR], nrm[D], f[NVAR];
-    // +N face of e (e is the minus element): own node at line end, neighbour's line start
-    {
-        const int im = G::template line_node<N>(m, P1 - 1);
-        load_state<D>(prm.u + (e * G::NN + im) * NVAR, ul);
-        const int nb = __ldg(prm.plus + N * prm.n_elem + e);
-        if (nb >= 0) load_state<D>(prm.u + ((long long)nb * G::NN + G::template line_node<N>(m, 0)) * NVAR, ur);
+    const int stride = G::stride(n);
+    const int hi = m / stride, lo = m - hi * stride;
+    const int first = hi * P1 * stride + lo;         // line position 0
+    const int last = first + (P1 - 1) * stride;      // line position p
+    double ul[NVAR], ur[NVAR], nrm[D];
+    if (side) {
+        load_state<D>(prm.u + (e * G::NN + last) * NVAR, ul);
+        const int nb = __ldg(prm.plus + n * prm.n_elem + e);
+        if (nb >= 0) load_state<D>(prm.u + ((long long)nb * G::NN + first) * NVAR, ur);
         else load_state<D>(prm.ghost_u + ((long long)(-nb - 1) * FN + m) * NVAR, ur);
         if constexpr (CURVED) {
 #pragma unroll
-            for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ja + ((e * G::NN + im) * D + N) * D + j);
-        } else {
-#pragma unroll
-            for (int j = 0; j < D; ++j) nrm[j] = (j == N) ? prm.areas[N] : 0.0;
+            for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
         }
-        face_flux<D, CURVED, MODE, N>(prm, ul, ur, nrm, f);
-        const double J = CURVED ? __ldg(prm.jac + e * G::NN + im) : prm.jac_const;
-        const double sm = 1.0 / (prm.wp * J);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, im)] += sm * f[v];
-    }
-    // -N face of e (e is the plus element): neighbour's line end, own line start
-    {
-        const int ip = G::template line_node<N>(m, 0);
-        const int nb = __ldg(prm.minus + N * prm.n_elem + e);
-        const int jm = G::template line_node<N>(m, P1 - 1);
+    } else {
+        const int nb = __ldg(prm.minus + n * prm.n_elem + e);
         if (nb >= 0) {
-            load_state<D>(prm.u + ((long long)nb * G::NN + jm) * NVAR, ul);
+            load_state<D>(prm.u + ((long long)nb * G::NN + last) * NVAR, ul);
             if constexpr (CURVED) {
 #pragma unroll
-                for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ja + (((long long)nb * G::NN + jm) * D + N) * D + j);
+                for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ja + (((long long)nb * G::NN + last) * D + n) * D + j);
             }
         } else {
             const long long g = -nb - 1;
@@ -263,29 +397,58 @@ __device__ __forceinline__ void surface_direction(const KParams& prm, double* sa
                 for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ghost_nrm + (g * FN + m) * D + j);
             }
         }
-        if constexpr (!CURVED) {
+        load_state<D>(prm.u + (e * G::NN + first) * NVAR, ur);
+    }
+    if constexpr (!CURVED) {
 #pragma unroll
-            for (int j = 0; j < D; ++j) nrm[j] = (j == N) ? prm.areas[N] : 0.0;
-        }
-        load_state<D>(prm.u + (e * G::NN + ip) * NVAR, ur);
-        face_flux<D, CURVED, MODE, N>(prm, ul, ur, nrm, f);
-        const double J = CURVED ? __ldg(prm.jac + e * G::NN + ip) : prm.jac_const;
-        const double sp = 1.0 / (prm.w0 * J);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, ip)] -= sp * f[v];
+        for (int j = 0; j < D; ++j) nrm[j] = (j == n) ? prm.areas[n] : 0.0;
+    }
+    switch (n) {
+    case 0: face_flux<D, CURVED, MODE, 0>(prm, ul, ur, nrm, f); break;
+    case 1: face_flux<D, CURVED, MODE, 1>(prm, ul, ur, nrm, f); break;
+    default: face_flux<D, CURVED, MODE, D - 1>(prm, ul, ur, nrm, f); break;
     }
 }
 
+#if FDG_PHASE_TIMING
+// profiling build only (scripts/variants.sh): SM cycles per phase, summed over CTAs/batches
+__device__ unsigned long long fdg_phase_cycles[8];
+extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, fdg_phase_cycles, sizeof(fdg_phase_cycles));
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(fdg_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#define FDG_PT(i)                          \
+    if (tid == 0) {                        \
+        const long long t_ = clock64();    \
+        pt_[i] += t_ - pt_last_;           \
+        pt_last_ = t_;                     \
+    }
+#else
+#define FDG_PT(i)
+#endif
+
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS>
-__global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_constant__ KParams prm)
+__global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(const __grid_constant__ KParams prm)
 {
     using G = Geo<D, P1>;
     constexpr int NN = G::NN, NVAR = G::NVAR, EPB = G::EPB, NT = G::NT;
     constexpr int NX = n_extra(VF, LOGS);
+    constexpr int KU = (EPB * NN * NVAR + NT - 1) / NT;  // state values per thread
+    constexpr int KN = (EPB * NN + NT - 1) / NT;         // nodes per thread
     extern __shared__ double smem[];
     double* sq = smem;                        // (2+D+NX) fields x FS
-    double* sacc = smem + (2 + D + NX) * G::FS;  // NVAR x FA (AoS u staging before the volume pass)
+    double* sacc = smem + sq_doubles<D, P1, VF, LOGS>();  // NVAR x FA (AoS u staging before the volume pass)
     const int tid = threadIdx.x;
+#if FDG_PHASE_TIMING
+    long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt_last_ = clock64();
+#endif
     const int el = tid / G::LINES;
     const int m = tid % G::LINES;
     const long long nbatch = (prm.n_elem + EPB - 1) / EPB;
@@ -299,98 +462,209 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT) elem_kernel(const __grid_const
         const long long e = e0 + el;
         const bool active = (el < ne);
 
+#if FDG_PREFETCH
+        // warm L2 with the next batch of this CTA (its state, and metrics on
+        // curved meshes) while this one computes: the next staging copy then
+        // waits on L2, not HBM, latency
+        {
+            const long long nb = batch + gridDim.x;
+            if (nb < nbatch) {
+                const long long ne2 = min((long long)EPB, prm.n_elem - nb * EPB);
+                const char* p0 = reinterpret_cast<const char*>(prm.u + nb * EPB * NN * NVAR);
+                const int bytes = (int)(ne2 * NN * NVAR * 8);
+                for (int off = tid * 128; off < bytes; off += NT * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + off));
+                if constexpr (CURVED) {
+                    const char* p1 = reinterpret_cast<const char*>(prm.ja + nb * EPB * NN * D * D);
+                    const int b1 = (int)(ne2 * NN * D * D * 8);
+                    for (int off = tid * 128; off < b1; off += NT * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(p1 + off));
+                }
+            }
+        }
+#endif
         if (epi != EPI_SURFACE) {
-            // ---- stage: coalesced copy (AoS), then primitives per node (SoA)
-            for (int t = tid; t < count; t += NT) sacc[t] = __ldg(prm.u + base + t);
-            __syncthreads();
-            for (int t = tid; t < ne * NN; t += NT) {
-                const int tel = t / NN, node = t - tel * NN;
-                const double* su = sacc + t * NVAR;
-                if (!gate_ok<D>(su, prm.gas.gm1))
-                    atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN + t));
-                const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
-                store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
+            // ---- stage: coalesced copy (AoS), then primitives per node (SoA).
+            // Compile-time trip counts: every load of the batch is in flight
+            // before the first shared-memory store, and the per-node chains
+            // (division, reciprocal, logs) of one thread run side by side.
+            FDG_PT(7)
+            {
+                constexpr int CH = KU < 24 ? KU : 16;
+#pragma unroll
+                for (int k0 = 0; k0 < KU; k0 += CH) {
+                    double tmp[CH];
+#pragma unroll
+                    for (int k = 0; k < CH; ++k) {
+                        const int t = tid + (k0 + k) * NT;
+                        tmp[k] = (k0 + k < KU && t < count) ? __ldg(prm.u + base + t) : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < CH; ++k) {
+                        const int t = tid + (k0 + k) * NT;
+                        if (k0 + k < KU && t < count) sacc[t] = tmp[k];
+                    }
+                }
             }
             __syncthreads();
+            FDG_PT(0)
+#pragma unroll(kStageUnroll)
+            for (int k = 0; k < KN; ++k) {
+                const int t = tid + k * NT;
+                if (t < ne * NN) {
+                    const int tel = t / NN, node = t - tel * NN;
+                    const double* su = sacc + t * NVAR;
+                    const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
+                    const bool ok = (MODE == FAST) ? gate_ok_fast<D>(su, 2.0 * q.p, prm.gas.gm1)
+                                                   : gate_ok<D>(su, prm.gas.gm1);
+                    if (!ok) atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN + t));
+                    store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
+                }
+            }
+            __syncthreads();
+            FDG_PT(1)
             // ---- volume integral, direction by direction (accumulators: SoA)
             if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e);
             __syncthreads();
+            FDG_PT(2)
             if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e);
             __syncthreads();
+            FDG_PT(3)
             if constexpr (D == 3) {
                 if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e);
                 __syncthreads();
             }
-            // ---- VOL = acc / J
-            for (int t = tid; t < count; t += NT) {
-                const int tel = t / (NN * NVAR);
-                const int r = t - tel * NN * NVAR;
-                const int node = r / NVAR, v = r - node * NVAR;
-                const double J = CURVED ? __ldg(prm.jac + (e0 + tel) * NN + node) : prm.jac_const;
-                const int s = G::acc(v, tel, node);
-                const double vol = sacc[s] / J;
-                if (epi == EPI_VOLUME) prm.out[base + t] = vol;
-                else sacc[s] = vol;
+            FDG_PT(4)
+            // ---- VOL = acc / J   (FAITHFUL: the reference's division, out /= jac;
+            //                       FAST: times 1/J)
+            // one thread per node: the Jacobian and index math once per node
+#pragma unroll
+            for (int k = 0; k < KN; ++k) {
+                const int t = tid + k * NT;
+                if (t < ne * NN) {
+                    const int tel = t / NN, node = t - tel * NN;
+                    double scale;
+                    if constexpr (MODE == FAST)
+                        scale = CURVED ? rcp_fast(__ldg(prm.jac + e0 * NN + t)) : prm.rjac_const;
+                    else
+                        scale = CURVED ? __ldg(prm.jac + e0 * NN + t) : prm.jac_const;
+#pragma unroll
+                    for (int v = 0; v < NVAR; ++v) {
+                        const int s = G::acc(v, tel, node);
+                        const double vol = (MODE == FAST) ? sacc[s] * scale : sacc[s] / scale;
+                        if (epi == EPI_VOLUME) prm.out[base + t * NVAR + v] = vol;
+                        else sacc[s] = vol;
+                    }
+                }
             }
             if (epi == EPI_VOLUME) {
                 __syncthreads();
+                FDG_PT(5)
                 continue;
             }
         } else {
             // mesh_surface: accumulate into the caller's array
-            for (int t = tid; t < count; t += NT) {
-                const int tel = t / (NN * NVAR);
-                const int r = t - tel * NN * NVAR;
-                const int node = r / NVAR, v = r - node * NVAR;
-                sacc[G::acc(v, tel, node)] = prm.out[base + t];
+#pragma unroll
+            for (int k = 0; k < KU; ++k) {
+                const int t = tid + k * NT;
+                if (t < count) {
+                    const int tel = t / (NN * NVAR);
+                    const int r = t - tel * NN * NVAR;
+                    const int node = r / NVAR, v = r - node * NVAR;
+                    sacc[G::acc(v, tel, node)] = prm.out[base + t];
+                }
             }
         }
         __syncthreads();
-        // ---- interface terms, direction by direction
-        if (active) surface_direction<D, P1, CURVED, MODE, 0>(prm, sacc, el, m, e);
-        __syncthreads();
-        if (active) surface_direction<D, P1, CURVED, MODE, 1>(prm, sacc, el, m, e);
-        __syncthreads();
-        if constexpr (D == 3) {
-            if (active) surface_direction<D, P1, CURVED, MODE, 2>(prm, sacc, el, m, e);
-            __syncthreads();
-        }
-        // ---- outputs
-        bool bad = false;
-        for (int t = tid; t < count; t += NT) {
-            const int tel = t / (NN * NVAR);
-            const int r = t - tel * NN * NVAR;
-            const int node = r / NVAR, v = r - node * NVAR;
-            const double val = sacc[G::acc(v, tel, node)];
-            if (epi == EPI_SURFACE) {
-                prm.out[base + t] = val;
-            } else if (epi == EPI_RHS) {
-                prm.out[base + t] = -val;
-            } else {  // EPI_STAGE
-                const double k = -val;
-                const double x = __ldg(prm.u + base + t);
-                double y;
-                if (prm.stage_kind == 0) {
-                    // du = a_i du + dt k ; v = v + b_i du     (timeint.py:157-158)
-                    // (a_0 == 0: the register starts at zero, nothing to read)
-                    double rg;
-                    if (prm.sa == 0.0) rg = prm.dt * k;
-                    else if constexpr (MODE == FAST) rg = fma(prm.sa, prm.reg[base + t], prm.dt * k);
-                    else rg = prm.sa * prm.reg[base + t] + prm.dt * k;
-                    prm.reg[base + t] = rg;
-                    y = x + prm.sb * rg;
-                } else {
-                    // y = (A u0 + B x) + (C dt) k             (Shu-Osher SSPRK43)
-                    const double s = (prm.sa != 0.0) ? prm.sa * __ldg(prm.u0 + base + t) + prm.sb * x : x;
-                    y = s + prm.sc * k;
+        // ---- interface fluxes: every face node of the batch independently
+        // (both sides of an interface evaluate it from identical arguments),
+        // into a face buffer that reuses the primitive-field region
+        {
+            constexpr int KF = (EPB * G::NF + NT - 1) / NT;
+            double* fbuf = sq;
+#pragma unroll 2
+            for (int k = 0; k < KF; ++k) {
+                const int it = tid + k * NT;
+                if (it < ne * G::NF) {
+                    const int fel = it / G::NF, r = it - fel * G::NF;
+                    const int f = r / G::LINES, mm = r - f * G::LINES;
+                    double fl[NVAR];
+                    face_flux_item<D, P1, CURVED, MODE>(prm, e0 + fel, f >> 1, f & 1, mm, fl);
+#pragma unroll
+                    for (int v = 0; v < NVAR; ++v) fbuf[it * NVAR + v] = fl[v];
                 }
-                prm.out[base + t] = y;
-                bad |= !isfinite(y);
+            }
+        }
+        __syncthreads();
+        // ---- per node: VOL + lifted face fluxes in direction order
+        // (discretization.py:754-760: out += 1/(w_p J) f on the minus side,
+        // out -= 1/(w_0 J) f on the plus side), then the outputs
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < KN; ++k) {
+            const int t = tid + k * NT;
+            if (t >= ne * NN) continue;
+            const int tel = t / NN, node = t - tel * NN;
+            double val[NVAR];
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) val[v] = sacc[G::acc(v, tel, node)];
+            const double J = CURVED ? __ldg(prm.jac + e0 * NN + t) : prm.jac_const;
+            const double* fb = sq + tel * G::NF * NVAR;
+#pragma unroll
+            for (int n = 0; n < D; ++n) {
+                const int stride = G::stride(n);
+                const int a = (node / stride) % P1;
+                const int ml = node / (stride * P1) * stride + node % stride;
+                if (a == P1 - 1) {
+                    const double sm = 1.0 / (prm.wp * J);
+                    const double* fv = fb + ((2 * n + 1) * G::LINES + ml) * NVAR;
+#pragma unroll
+                    for (int v = 0; v < NVAR; ++v) val[v] += sm * fv[v];
+                }
+                if (a == 0) {
+                    const double sp = 1.0 / (prm.w0 * J);
+                    const double* fv = fb + ((2 * n) * G::LINES + ml) * NVAR;
+#pragma unroll
+                    for (int v = 0; v < NVAR; ++v) val[v] -= sp * fv[v];
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                const long long g = base + (long long)t * NVAR + v;
+                if (epi == EPI_SURFACE) {
+                    prm.out[g] = val[v];
+                } else if (epi == EPI_RHS) {
+                    prm.out[g] = -val[v];
+                } else {  // EPI_STAGE
+                    const double kv = -val[v];
+                    const double x = __ldg(prm.u + g);
+                    double y;
+                    if (prm.stage_kind == 0) {
+                        // du = a_i du + dt k ; v = v + b_i du     (timeint.py:157-158)
+                        // (a_0 == 0: the register starts at zero, nothing to read)
+                        double rg;
+                        if (prm.sa == 0.0) rg = prm.dt * kv;
+                        else if constexpr (MODE == FAST) rg = fma(prm.sa, prm.reg[g], prm.dt * kv);
+                        else rg = prm.sa * prm.reg[g] + prm.dt * kv;
+                        prm.reg[g] = rg;
+                        y = x + prm.sb * rg;
+                    } else {
+                        // y = (A u0 + B x) + (C dt) k             (Shu-Osher SSPRK43)
+                        const double s = (prm.sa != 0.0) ? prm.sa * __ldg(prm.u0 + g) + prm.sb * x : x;
+                        y = s + prm.sc * kv;
+                    }
+                    prm.out[g] = y;
+                    bad |= !isfinite(y);
+                }
             }
         }
         if (bad) atomicMin(&prm.status->bad_stage, prm.stage_index);
         __syncthreads();
     }
+#if FDG_PHASE_TIMING
+    if (tid == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(&fdg_phase_cycles[i], (unsigned long long)pt_[i]);
+#endif
 }
 
 }  // namespace fdg

@@ -327,3 +327,48 @@ def test_device_stepper_graph_and_divergence():
     bad[2, 3, 0] = -1.0
     with pytest.raises(P.AdmissibilityError, match="element 2, node 3"):
         st.step(bad, 1e-3)
+
+
+# --------------------------------------------------- partitioned device path
+
+
+@pytest.mark.parametrize("world,dims,p,amp", [(2, (4, 2, 3), 3, 0.0), (3, (6, 2, 2), 4, -0.1), (2, (4, 5), 3, 0.1)])
+@pytest.mark.parametrize("kernel", ["reference", "batched"])
+def test_slab_partition_on_device_bitwise(world, dims, p, amp, kernel):
+    """The ghost-slot path of the element kernel: W slabs on one GPU, face
+    traces packed with fdg_pack_faces and handed over by device copies (the
+    NCCL exchange moves exactly these buffers), RHS of every slab bitwise equal
+    to the single-domain RHS."""
+    import torch
+
+    P = _pkg()
+    from paper_2112_10517_b200.device import DeviceMesh
+    from paper_2112_10517_b200.parallel import slab_partition
+
+    gas = P.GasParams(1.4)
+    setup = P.build_setup(P.build_mesh(dims, bounds=(-1.0, 1.0), amplitude=amp), P.lgl_operator(p), gas)
+    rng = np.random.default_rng(3)
+    q = np.empty((setup.n_elements, setup.n_nodes, setup.d + 2))
+    q[..., 0] = 1.0 + 0.3 * rng.random(q.shape[:2])
+    q[..., 1 : setup.d + 1] = 0.3 * (rng.random(q.shape[:2] + (setup.d,)) - 0.5)
+    q[..., -1] = 1.0 + 0.3 * rng.random(q.shape[:2])
+    u = P.prim2cons(q, gas)
+    cfg = P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel=kernel)
+    want = P.rhs(u, setup, cfg)
+    parts = [slab_partition(setup, r, world) for r in range(world)]
+    dms = [DeviceMesh(setup, partition=pt) for pt in parts]
+    us = [torch.as_tensor(np.ascontiguousarray(u[pt["lo"] : pt["hi"]]), device="cuda") for pt in parts]
+    fn = (p + 1) ** (setup.d - 1)
+    first, last = [], []
+    for dm, pt, ul in zip(dms, parts, us):
+        F = pt["plane"]
+        a = torch.empty((F, fn, setup.d + 2), dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        dm.pack_faces(ul, torch.as_tensor(pt["send_first"], device="cuda"), 0, 0, a)
+        dm.pack_faces(ul, torch.as_tensor(pt["send_last"], device="cuda"), 0, 1, b)
+        first.append(a)
+        last.append(b)
+    for r, (dm, pt, ul) in enumerate(zip(dms, parts, us)):
+        ghost = torch.cat([first[(r + 1) % world], last[(r - 1) % world]])
+        got = dm.rhs(ul, cfg.scheme(), ghost_u=ghost).cpu().numpy()
+        assert np.array_equal(got, want[pt["lo"] : pt["hi"]]), r
