@@ -209,6 +209,93 @@ def _traffic_from_profile():
     return None
 
 
+def run_sharded(args, rank, world, local, dist):
+    """Full RHS (or SSPRK43 step) of cfg4 / cfg5, slab-partitioned over the
+    ranks with the NCCL face-trace halo every RHS (strong scaling)."""
+    import torch
+
+    from paper_2112_10517_b200 import _native as N
+    from paper_2112_10517_b200 import workloads
+    from paper_2112_10517_b200.device import DeviceMesh
+    from paper_2112_10517_b200.parallel import HaloExchange, slab_partition
+    from paper_2112_10517_b200.timeint import SSPRK43, DeviceStepper
+
+    cfg = {"rhs4": 4, "rhs5": 5, "step4": 4}[args.workload]
+    setup, u_host, config = workloads.build(cfg, kernel="batched")
+    part = slab_partition(setup, rank, world)
+    dm = DeviceMesh(setup, partition=part)
+    lo, hi = part["lo"], part["hi"]
+    u = torch.as_tensor(np.ascontiguousarray(u_host[lo:hi]), device="cuda")
+    nodes_total = u_host.shape[0] * u_host.shape[1]
+    del u_host
+    halo = HaloExchange(part, setup.d, setup.op.degree + 1, torch, dist, device="cuda", pack=dm.pack_faces) \
+        if world > 1 else None
+    scheme = config.scheme()
+    out = dm.empty()
+    stepper = None
+    if args.workload == "step4":
+        stepper = DeviceStepper(dm, config, SSPRK43, exchange=halo)
+        dt = 1e-4
+
+    def step():
+        if stepper is not None:
+            return stepper.step(u, dt, check=False)
+        ghost = halo(u) if halo is not None else None
+        return dm.rhs(u, scheme, out=out, ghost_u=ghost)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    launches0 = N.launch_count()
+    with ClockSampler(local) as clocks:
+        a.record(stream)
+        for _ in range(args.steps):
+            step()
+        b.record(stream)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    ms = a.elapsed_time(b) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rhs_per_step = 4 if stepper is not None else 1
+    value = nodes_total * rhs_per_step / (ms * 1e-3)
+    line = {
+        "metric": "full-RHS DOF updates/s (1/PID), fp64",
+        "value": value,
+        "unit": "DOF/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": "cfg%d %s: %s" % (cfg, args.workload, workloads.CONFIGS[cfg]),
+            "nodes_total": nodes_total,
+            "partition": "x-slabs of the element index, NCCL grouped send/recv of face traces per RHS",
+            "l2": "inputs larger than L2 (%.0f MB state)" % (nodes_total * 5 * 8 / 1e6),
+            "rhs_per_step": rhs_per_step,
+        },
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -216,6 +303,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="vol2", choices=["vol2", "rhs4", "rhs5", "step4"],
+                    help="vol2: the headline (BASELINE configs[1]); rhs4/rhs5: sharded full RHS of cfg4/cfg5 "
+                         "(strong scaling, NCCL face-trace halo); step4: sharded SSPRK43 step of cfg4")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
@@ -234,6 +324,8 @@ def main():
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload != "vol2":
+        return run_sharded(args, rank, world, local, dist)
 
     from paper_2112_10517_b200 import _native as N
     from paper_2112_10517_b200 import workloads

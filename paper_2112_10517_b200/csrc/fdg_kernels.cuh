@@ -82,6 +82,10 @@ struct KParams {
 #define FDG_STAGE_UNROLL 2
 #endif
 constexpr int kStageUnroll = FDG_STAGE_UNROLL;
+#ifndef FDG_FACE_UNROLL
+#define FDG_FACE_UNROLL 2
+#endif
+constexpr int kFaceUnroll = FDG_FACE_UNROLL;
 #ifndef FDG_PAD
 #define FDG_PAD 1
 #endif
@@ -352,7 +356,19 @@ __device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, 
         if constexpr (MODE == FAST) flux_llf_fast<D, CURVED ? -1 : N>(ul, ur, nrm, prm.gas, f);
         else flux_llf<D, MODE>(ul, ur, nrm, prm.gas, f);
     } else {
-        surface_flux<D, MODE>(prm.surface_flux, ul, ur, nrm, prm.gas, f);
+        // copies: only these arrays have their address taken by the
+        // out-of-line call, the caller's stay in registers
+        double a[D + 2], b[D + 2], nn[D], g[D + 2];
+#pragma unroll
+        for (int v = 0; v < D + 2; ++v) {
+            a[v] = ul[v];
+            b[v] = ur[v];
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) nn[j] = nrm[j];
+        surface_flux<D, MODE>(prm.surface_flux, a, b, nn, prm.gas, g);
+#pragma unroll
+        for (int v = 0; v < D + 2; ++v) f[v] = g[v];
     }
 }
 
@@ -403,16 +419,15 @@ __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, 
 #pragma unroll
         for (int j = 0; j < D; ++j) nrm[j] = (j == n) ? prm.areas[n] : 0.0;
     }
-    switch (n) {
-    case 0: face_flux<D, CURVED, MODE, 0>(prm, ul, ur, nrm, f); break;
-    case 1: face_flux<D, CURVED, MODE, 1>(prm, ul, ur, nrm, f); break;
-    default: face_flux<D, CURVED, MODE, D - 1>(prm, ul, ur, nrm, f); break;
-    }
+    // one general-normal code path for every direction (a Cartesian face is
+    // the normal area e_n): keeps the RHS kernel inside the instruction cache
+    face_flux<D, true, MODE, 0>(prm, ul, ur, nrm, f);
 }
 
 #if FDG_PHASE_TIMING
 // profiling build only (scripts/variants.sh): SM cycles per phase, summed over CTAs/batches
 __device__ unsigned long long fdg_phase_cycles[8];
+__device__ unsigned long long fdg_cta_ns[2 * 8192];  // per-CTA globaltimer start/end (first launch after reset)
 extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
 {
     cudaDeviceSynchronize();
@@ -421,6 +436,12 @@ extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
         unsigned long long z[8] = {0};
         cudaMemcpyToSymbol(fdg_phase_cycles, z, sizeof(z));
     }
+    return 0;
+}
+extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, fdg_cta_ns, sizeof(unsigned long long) * 2 * n);
     return 0;
 }
 #define FDG_PT(i)                          \
@@ -448,6 +469,8 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(
 #if FDG_PHASE_TIMING
     long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long pt_last_ = clock64();
+    unsigned long long ns0_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns0_));
 #endif
     const int el = tid / G::LINES;
     const int m = tid % G::LINES;
@@ -582,7 +605,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(
         {
             constexpr int KF = (EPB * G::NF + NT - 1) / NT;
             double* fbuf = sq;
-#pragma unroll 2
+#pragma unroll(kFaceUnroll)
             for (int k = 0; k < KF; ++k) {
                 const int it = tid + k * NT;
                 if (it < ne * G::NF) {
@@ -600,7 +623,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(
         // (discretization.py:754-760: out += 1/(w_p J) f on the minus side,
         // out -= 1/(w_0 J) f on the plus side), then the outputs
         bool bad = false;
-#pragma unroll
+#pragma unroll 1
         for (int k = 0; k < KN; ++k) {
             const int t = tid + k * NT;
             if (t >= ne * NN) continue;
@@ -664,6 +687,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(
 #if FDG_PHASE_TIMING
     if (tid == 0)
         for (int i = 0; i < 8; ++i) atomicAdd(&fdg_phase_cycles[i], (unsigned long long)pt_[i]);
+    if (tid == 0 && blockIdx.x < 8192) {
+        unsigned long long ns1_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1_));
+        fdg_cta_ns[2 * blockIdx.x] = ns0_;
+        fdg_cta_ns[2 * blockIdx.x + 1] = ns1_;
+    }
 #endif
 }
 

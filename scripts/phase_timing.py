@@ -31,3 +31,27 @@ for dims in [(16, 16, 16), (64, 64, 64)]:
     batches = 5 * (setup.n_elements // 8)
     print(dims, "cycles per batch per CTA:", {n: round(buf[i] / batches) for i, n in enumerate(names) if buf[i]},
           "total", round(tot / batches))
+
+# per-CTA start/end (globaltimer) of one cfg2 launch
+L.fdg_debug_cta_ns.argtypes = [ctypes.c_void_p, ctypes.c_int]
+setup, u_host, cfg = workloads.build(2, kernel="batched")
+dm = DeviceMesh(setup)
+u = torch.as_tensor(u_host, device="cuda")
+out = dm.empty()
+s = cfg.scheme()
+for _ in range(3):
+    dm.volume(u, s, out=out)
+torch.cuda.synchronize()
+flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+flush.sum()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record(); dm.volume(u, s, out=out); e1.record(); torch.cuda.synchronize()
+n = 1024
+buf = (ctypes.c_ulonglong * (2 * n))()
+L.fdg_debug_cta_ns(buf, n)
+import numpy as np
+a = np.array(buf[:], dtype=np.float64).reshape(n, 2)
+t0 = a[:, 0].min()
+st, en = a[:, 0] - t0, a[:, 1] - t0
+print("event ms %.4f | CTA start: min %.0f med %.0f max %.0f ns | end: min %.0f med %.0f max %.0f ns | dur med %.0f max %.0f"
+      % (e0.elapsed_time(e1), st.min(), np.median(st), st.max(), en.min(), np.median(en), en.max(), np.median(en - st), (en - st).max()))

@@ -20,10 +20,6 @@ nvcc $COMMON -c obj_var/stubs.cu -o obj_var/stubs.o &
 nvcc $COMMON -c fdg_capi.cu -o obj_var/capi.o &
 nvcc $COMMON -c fdg_probe.cu -o obj_var/probe.o &
 declare -A FLAGS=(
-  [base]=""
-  [t64_b7]="-DFDG_TARGET_THREADS=64 -DFDG_MIN_BLOCKS=7"
-  [t64_b6]="-DFDG_TARGET_THREADS=64 -DFDG_MIN_BLOCKS=6"
-  [t96_b5]="-DFDG_TARGET_THREADS=96 -DFDG_MIN_BLOCKS=5"
   [pt]="-DFDG_PHASE_TIMING=1"
 )
 FMAD=--fmad=true; [[ $UNIT == faithful* ]] && FMAD=--fmad=false
