@@ -107,6 +107,23 @@ void fdg_mesh_destroy(fdg_mesh_t *mesh);
 
 /* VOL = (1/J) sum_n sum_k Dsplit f*_n(u_i, u_k)   (not negated) */
 int fdg_volume(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, double *vol, void *stream);
+/* the same for elements [elem_lo, elem_hi) only (u, vol: the whole arrays);
+ * the volume integral is element-local, so host<->device copies of element
+ * chunks can be pipelined against it (batched.py:450-511 processes any block
+ * of elements independently as well) */
+int fdg_volume_range(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, double *vol, int64_t elem_lo,
+                     int64_t elem_hi, void *stream);
+/* fdg_volume on a HOST state into a HOST buffer (the call an FFI user with
+ * numpy arrays makes; batched.py:450-511 takes and returns host arrays):
+ * element chunks are copied in on one library-owned stream, integrated on
+ * `stream`, copied out on another, so both copy directions and the SMs work
+ * concurrently.  u_host/vol_host should be pinned (pageable memory works but
+ * serializes the copies); u_dev/vol_dev are caller-owned device scratch of the
+ * state's size.  n_chunks <= 0 picks >= 4 MB chunks (2..16).  Asynchronous: `stream`
+ * is ordered after the last copy-out, so synchronizing it (or
+ * fdg_read_status) completes the call. */
+int fdg_volume_host(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u_host, double *vol_host,
+                    double *u_dev, double *vol_dev, int32_t n_chunks, void *stream);
 /* out += SURF  (LGL interface terms, lifted and /J) */
 int fdg_surface(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, const double *ghost_u,
                 double *out, void *stream);

@@ -80,6 +80,8 @@ EXPORTS = (
     "fdg_mesh_create",
     "fdg_mesh_destroy",
     "fdg_volume",
+    "fdg_volume_range",
+    "fdg_volume_host",
     "fdg_surface",
     "fdg_rhs",
     "fdg_rk_stage",
@@ -115,6 +117,8 @@ def lib():
     L.fdg_mesh_destroy.argtypes = [vp]
     L.fdg_mesh_destroy.restype = None
     L.fdg_volume.argtypes = [vp, P(Scheme), vp, vp, vp]
+    L.fdg_volume_range.argtypes = [vp, P(Scheme), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
+    L.fdg_volume_host.argtypes = [vp, P(Scheme), vp, vp, vp, vp, i32, vp]
     L.fdg_surface.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rhs.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rk_stage.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, vp]

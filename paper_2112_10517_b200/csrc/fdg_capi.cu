@@ -11,6 +11,8 @@
 
 using namespace fdg;
 
+static constexpr int kMaxChunks = 32;
+
 struct fdg_mesh {
     int d = 0, p1 = 0;
     long long n_elem = 0;
@@ -18,6 +20,10 @@ struct fdg_mesh {
     int sm_count = 148;
     KParams base{};
     Status* status = nullptr;  // device
+    // host-buffer pipeline (fdg_volume_host): two copy streams + events, made on first use
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_k[kMaxChunks] = {};
 };
 
 static thread_local std::string g_last_error;
@@ -126,6 +132,14 @@ void fdg_mesh_destroy(fdg_mesh_t* m)
 {
     if (!m) return;
     if (m->status) cudaFree(m->status);
+    if (m->s_in) cudaStreamDestroy(m->s_in);
+    if (m->s_out) cudaStreamDestroy(m->s_out);
+    for (cudaEvent_t e : {m->ev_start, m->ev_done})
+        if (e) cudaEventDestroy(e);
+    for (int c = 0; c < kMaxChunks; ++c) {
+        if (m->ev_in[c]) cudaEventDestroy(m->ev_in[c]);
+        if (m->ev_k[c]) cudaEventDestroy(m->ev_k[c]);
+    }
     delete m;
 }
 
@@ -187,6 +201,111 @@ int fdg_volume(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, double* vo
     k.precompute = s->precompute;
     k.surface_flux = F_LLF;
     return run(m, s, k, s->volume_flux, stream);
+}
+
+static long long nodes_per_elem(const fdg_mesh* m)
+{
+    long long nn = 1;
+    for (int i = 0; i < m->d; ++i) nn *= m->p1;
+    return nn;
+}
+
+// volume kernel on elements [lo, hi): pointers shifted, element ids kept global
+static int volume_range(fdg_mesh* m, const fdg_scheme_t* s, LaunchFn fn, const double* u, double* vol, long long lo,
+                        long long hi, cudaStream_t stream)
+{
+    if (lo == hi) return FDG_OK;
+    const long long nn = nodes_per_elem(m);
+    const long long nvar = m->d + 2;
+    KParams k = m->base;
+    k.u = u + lo * nn * nvar;
+    k.out = vol + lo * nn * nvar;
+    if (k.ja) k.ja += lo * nn * m->d * m->d;
+    if (k.jac) k.jac += lo * nn;
+    k.n_elem = hi - lo;
+    k.elem_base += lo;
+    k.epilogue = EPI_VOLUME;
+    k.precompute = s->precompute;
+    k.surface_flux = F_LLF;
+    cudaError_t err = fn(k, stream, m->sm_count);
+    if (err != cudaSuccess) return cuda_fail(err, "element kernel launch");
+    g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_volume_range(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, double* vol, int64_t lo, int64_t hi,
+                     void* stream)
+{
+    if (!m || !u || !vol) return fail(FDG_ERR_ARG, "fdg_volume_range: null argument");
+    if (lo < 0 || hi > m->n_elem || lo > hi) return fail(FDG_ERR_ARG, "fdg_volume_range: bad range [%lld, %lld)",
+                                                          (long long)lo, (long long)hi);
+    int rc = check_scheme(s, true, false);
+    if (rc) return rc;
+    LaunchFn fn = find(m, s, s->volume_flux);
+    if (!fn) return fail(FDG_ERR_UNSUPPORTED, "no kernel for d=%d, p=%d", m->d, m->p1 - 1);
+    return volume_range(m, s, fn, u, vol, lo, hi, (cudaStream_t)stream);
+}
+
+static int pipeline_init(fdg_mesh* m)
+{
+    if (m->s_in) return FDG_OK;
+    cudaError_t err = cudaSuccess;
+    auto ev = [&](cudaEvent_t* e) {
+        if (err == cudaSuccess) err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    };
+    ev(&m->ev_start);
+    ev(&m->ev_done);
+    for (int c = 0; c < kMaxChunks; ++c) {
+        ev(&m->ev_in[c]);
+        ev(&m->ev_k[c]);
+    }
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&m->s_out, cudaStreamNonBlocking);
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&m->s_in, cudaStreamNonBlocking);
+    if (err != cudaSuccess) return cuda_fail(err, "pipeline streams/events");
+    return FDG_OK;
+}
+
+int fdg_volume_host(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u_host, double* vol_host, double* u_dev,
+                    double* vol_dev, int32_t n_chunks, void* stream)
+{
+    if (!m || !u_host || !vol_host || !u_dev || !vol_dev) return fail(FDG_ERR_ARG, "fdg_volume_host: null argument");
+    int rc = check_scheme(s, true, false);
+    if (rc) return rc;
+    LaunchFn fn = find(m, s, s->volume_flux);
+    if (!fn) return fail(FDG_ERR_UNSUPPORTED, "no kernel for d=%d, p=%d", m->d, m->p1 - 1);
+    if (m->n_elem == 0) return FDG_OK;
+    rc = pipeline_init(m);
+    if (rc) return rc;
+    const long long elem_bytes = nodes_per_elem(m) * (m->d + 2) * (long long)sizeof(double);
+    // default: >= 4 MB chunks, 2..16 of them.  Every chunk costs ~20 us of copy
+    // setup on B200/PCIe5 (profiles/r01_e2e.md: 2 chunks beat 10 on a 10 MB state)
+    if (n_chunks <= 0) n_chunks = (int32_t)std::max<long long>(2, std::min<long long>(16, m->n_elem * elem_bytes >> 22));
+    n_chunks = (int32_t)std::min<long long>(std::min<long long>(n_chunks, kMaxChunks), m->n_elem);
+    cudaStream_t st = (cudaStream_t)stream;
+    // both copy streams start after everything already queued on `stream`
+    cudaError_t err = cudaEventRecord(m->ev_start, st);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(m->s_in, m->ev_start, 0);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(m->s_out, m->ev_start, 0);
+    for (int c = 0; c < n_chunks && err == cudaSuccess; ++c) {
+        const long long lo = m->n_elem * c / n_chunks, hi = m->n_elem * (c + 1) / n_chunks;
+        const size_t off = (size_t)(lo * elem_bytes / (long long)sizeof(double));
+        const size_t bytes = (size_t)((hi - lo) * elem_bytes);
+        err = cudaMemcpyAsync(u_dev + off, u_host + off, bytes, cudaMemcpyHostToDevice, m->s_in);
+        if (err == cudaSuccess) err = cudaEventRecord(m->ev_in[c], m->s_in);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(st, m->ev_in[c], 0);
+        if (err != cudaSuccess) break;
+        rc = volume_range(m, s, fn, u_dev, vol_dev, lo, hi, st);
+        if (rc) return rc;
+        err = cudaEventRecord(m->ev_k[c], st);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(m->s_out, m->ev_k[c], 0);
+        if (err == cudaSuccess)
+            err = cudaMemcpyAsync(vol_host + off, vol_dev + off, bytes, cudaMemcpyDeviceToHost, m->s_out);
+    }
+    // `stream` resumes after the last D2H copy
+    if (err == cudaSuccess) err = cudaEventRecord(m->ev_done, m->s_out);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(st, m->ev_done, 0);
+    if (err != cudaSuccess) return cuda_fail(err, "host pipeline");
+    return FDG_OK;
 }
 
 int fdg_surface(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* out,

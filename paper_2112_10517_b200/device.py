@@ -158,6 +158,48 @@ class DeviceMesh:
         N.check(N.lib().fdg_volume(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(out), _stream_handle(stream)))
         return out
 
+    def volume_range(self, u, scheme, out, lo, hi, stream=None):
+        """VOL of local elements [lo, hi) only; u and out are the whole arrays."""
+        N.check(
+            N.lib().fdg_volume_range(
+                self.handle, ctypes.byref(scheme), _ptr(u), _ptr(out), int(lo), int(hi), _stream_handle(stream)
+            )
+        )
+        return out
+
+    def volume_host(self, u_host, scheme, out_host, n_chunks=0, stream=None):
+        """VOL of a pinned host state into a pinned host buffer through
+        fdg_volume_host: the H2D copy of chunk c+1, the kernel on chunk c and
+        the D2H copy of chunk c-1 overlap. Ordered on ``stream`` (default: the
+        current one), which resumes after the last copy-out, so events
+        recorded around this call bracket the whole transfer. Returns the
+        device copy of the state (for error reports) and ``out_host``."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        u_dev = self._scratch("u_dev")
+        v_dev = self._scratch("v_dev")
+        last = self._staging.get("_scratch_done")
+        if last is not None:
+            s.wait_event(last)  # scratch reuse after a call on another stream
+        N.check(
+            N.lib().fdg_volume_host(
+                self.handle, ctypes.byref(scheme), _ptr(u_host), _ptr(out_host), _ptr(u_dev), _ptr(v_dev),
+                int(n_chunks), ctypes.c_void_p(s.cuda_stream),
+            )
+        )
+        if last is None:
+            last = self._staging["_scratch_done"] = torch.cuda.Event()
+        last.record(s)
+        return u_dev, out_host
+
+    def _scratch(self, key):
+        """Device buffer of the state's size, reused across calls."""
+        buf = self._staging.get(key)
+        if buf is None:
+            buf = self.empty()
+            self._staging[key] = buf
+        return buf
+
     def surface(self, u, scheme, out, ghost_u=None, stream=None):
         N.check(
             N.lib().fdg_surface(

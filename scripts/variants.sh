@@ -20,7 +20,8 @@ nvcc $COMMON -c obj_var/stubs.cu -o obj_var/stubs.o &
 nvcc $COMMON -c fdg_capi.cu -o obj_var/capi.o &
 nvcc $COMMON -c fdg_probe.cu -o obj_var/probe.o &
 declare -A FLAGS=(
-  [pt]="-DFDG_PHASE_TIMING=1"
+  [base]=""
+  [fu1]="-DFDG_FACE_UNROLL=1"
 )
 FMAD=--fmad=true; [[ $UNIT == faithful* ]] && FMAD=--fmad=false
 for name in "${!FLAGS[@]}"; do

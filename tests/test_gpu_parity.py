@@ -266,6 +266,41 @@ def test_gate_names_first_bad_node():
         P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(kernel="batched"))
 
 
+@pytest.mark.parametrize("kernel", ["reference", "batched"])
+def test_pinned_pipeline_matches_device_path(kernel):
+    """Pinned host state -> chunked H2D / fdg_volume_range / D2H pipeline:
+    bitwise equal to one whole-mesh launch (the volume integral is element-local)."""
+    P = _pkg()
+    import torch
+    from paper_2112_10517_b200 import workloads
+
+    setup, u, _ = workloads.build(2, dims=(16, 16, 12))  # 7.9 MB: several 2 MB chunks
+    cfg = P.RhsConfig(volume_flux="ranocha", precompute="primitives_and_logs", kernel=kernel)
+    want = P.mesh_fluxdiff_volume(torch.as_tensor(u, device="cuda"), setup, cfg).cpu().numpy()
+    u_pin = torch.from_numpy(u).pin_memory()
+    out_pin = torch.full(u.shape, np.nan, dtype=torch.float64).pin_memory()
+    dm = P.device.device_mesh_for(setup)
+    before = P._native.launch_count()
+    got = P.mesh_fluxdiff_volume(u_pin, setup, cfg, out=out_pin)
+    assert got.data_ptr() == out_pin.data_ptr()
+    assert P._native.launch_count() - before > 1  # several element chunks
+    assert np.array_equal(out_pin.numpy(), want)
+    got2 = P.mesh_fluxdiff_volume(u_pin, setup, cfg)  # no out: fresh host tensor
+    assert np.array_equal(got2.numpy(), want)
+    # explicit ranges tile the mesh
+    ud = torch.as_tensor(u, device="cuda")
+    vd = torch.full_like(ud, np.nan)
+    for lo, hi in ((0, 1), (1, 100), (100, 100), (100, dm.n_elem)):
+        dm.volume_range(ud, cfg.scheme(), vd, lo, hi)
+    assert np.array_equal(vd.cpu().numpy(), want)
+    with pytest.raises(Exception, match="bad range"):
+        dm.volume_range(ud, cfg.scheme(), vd, 5, dm.n_elem + 1)
+    bad = u.copy()
+    bad[300, 3, 0] = -1.0
+    with pytest.raises(P.AdmissibilityError, match="cons2prim"):
+        P.mesh_fluxdiff_volume(torch.from_numpy(bad).pin_memory(), setup, cfg, out=out_pin)
+
+
 # ------------------------------------------------------------ time stepping
 
 
