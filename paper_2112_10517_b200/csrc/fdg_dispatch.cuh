@@ -8,25 +8,60 @@ namespace fdg {
 
 using LaunchFn = cudaError_t (*)(const KParams&, cudaStream_t, int sm_count);
 
+// High-occupancy twin: FAST 3D kernels with P1 <= 5 are also built with an
+// 8-CTA register cap (128 regs at 64 threads). The default (6 CTAs, 168 regs)
+// is 4% faster per element in steady state, but when a launch fits in one wave
+// only at the higher occupancy (cfg2: 1024 batches vs 888 / 1184 slots) the
+// twin removes the second, mostly empty wave: cfg2 VOL 20.4 -> 18.4 us, RHS
+// 51 -> 39 us (profiles/r01_tuning.md).
+#ifndef FDG_HIOCC
+#define FDG_HIOCC 8
+#endif
+template <int D, int P1, int MODE>
+constexpr bool has_hiocc()
+{
+    return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && FDG_MIN_BLOCKS == 0;
+}
+
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC>
+cudaError_t elem_occupancy(int* blocks_per_sm)
+{
+    using G = Geo<D, P1>;
+    constexpr size_t smem = (size_t)smem_doubles<D, P1, VF, LOGS>() * sizeof(double);
+    auto kern = elem_kernel<D, P1, VF, CURVED, MODE, LOGS, OCC>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    int b = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, G::NT, smem);
+    *blocks_per_sm = std::max(1, b);
+    return err;
+}
+
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS>
 cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
 {
     using G = Geo<D, P1>;
     constexpr size_t smem = (size_t)smem_doubles<D, P1, VF, LOGS>() * sizeof(double);
-    auto kern = elem_kernel<D, P1, VF, CURVED, MODE, LOGS>;
-    static int blocks_per_sm = -1;  // one device per process
-    if (blocks_per_sm < 0) {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr bool twin = has_hiocc<D, P1, MODE>();
+    static int bps = -1, bps_hi = -1;  // resident CTAs per SM (one device per process)
+    if (bps < 0) {
+        cudaError_t err = elem_occupancy<D, P1, VF, CURVED, MODE, LOGS, 0>(&bps);
         if (err != cudaSuccess) return err;
-        int b = 0;
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, G::NT, smem);
-        if (err != cudaSuccess) return err;
-        blocks_per_sm = std::max(1, b);
+        if constexpr (twin) {
+            err = elem_occupancy<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>(&bps_hi);
+            if (err != cudaSuccess) return err;
+        }
     }
     const long long nb = (p.n_elem + G::EPB - 1) / G::EPB;
     if (nb <= 0) return cudaSuccess;
-    const long long grid = std::min(nb, (long long)blocks_per_sm * sm_count);
-    kern<<<(unsigned)grid, G::NT, smem, s>>>(p);
+    const long long slots = (long long)bps * sm_count;
+    if constexpr (twin) {
+        if (nb > slots && nb <= (long long)bps_hi * sm_count) {
+            elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC><<<(unsigned)nb, G::NT, smem, s>>>(p);
+            return cudaGetLastError();
+        }
+    }
+    elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0><<<(unsigned)std::min(nb, slots), G::NT, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -454,8 +454,11 @@ extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 #define FDG_PT(i)
 #endif
 
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS>
-__global__ void __launch_bounds__(Geo<D, P1>::NT, Geo<D, P1>::MINB) elem_kernel(const __grid_constant__ KParams prm)
+// OCC > 0 overrides the resident-CTA hint (the high-occupancy twin used when a
+// launch fits one wave only at that occupancy, fdg_dispatch.cuh)
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0>
+__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MINB)
+    elem_kernel(const __grid_constant__ KParams prm)
 {
     using G = Geo<D, P1>;
     constexpr int NN = G::NN, NVAR = G::NVAR, EPB = G::EPB, NT = G::NT;
