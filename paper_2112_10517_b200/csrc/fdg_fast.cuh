@@ -20,6 +20,56 @@
 
 namespace fdg {
 
+// Literal FP64 constants of the FAST path live in the constant bank, where
+// DFMA/DMUL take them as c[3][...] operands; a literal double in the
+// instruction stream costs two UMOVs per use (5.9% of the cfg2 kernel's
+// instructions before this table).
+enum FastConst {
+    KC_LOG1, KC_LOG2, KC_LOG3, KC_LOG4, KC_LOG5, KC_LOG6, KC_LOG7,  // log_fast T(z) coefficients
+    KC_LN2_HI, KC_LN2_LO,
+    KC_LM3, KC_LM5, KC_LM7,  // log-mean series 2/3, 2/5, 2/7 (means.py:16-40)
+    KC_SERIES_SQRT,          // sqrt(SERIES_EPSILON): u < 1e-4  <=>  |d| < 0.01 s
+    KC_COUNT
+};
+static __constant__ double kFast[KC_COUNT] = {
+    0.6666666666666734, 0.39999999999417485, 0.2857142874173421, 0.22222198640440488,
+    0.1818356087762256, 0.15314136991810745, 0.14795104806627174,
+    0.6931471805599453, 2.3190468138462996e-17,
+    2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0,
+    0.01,
+};
+
+// FAST natural log of a positive normal double, ~1.2 ulp (libdevice's log
+// costs ~86 instructions per call here, 20% of the cfg2 kernel; this one ~28).
+// x = 2^e m, m in [sqrt(1/2), sqrt(2)); log m = f - s (f - T(z)), f = m - 1
+// (exact), s = f / (2 + f), z = s^2, T(z) = 2 (atanh(s)/s - 1) fitted to
+// degree 7 (scripts/gen_logfast.py: coefficients and the error check).
+// Zero, negative, subnormal, inf and NaN arguments take libdevice's log.
+static __device__ __noinline__ double log_slow(double x) { return log(x); }
+
+__device__ __forceinline__ double log_fast(double x)
+{
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    if (hi < 0x00100000 || hi >= 0x7ff00000) return log_slow(x);  // out of line: keeps the pair loops small
+    const int e = (hi - 0x3fe6a09e) >> 20;  // 0x3fe6a09e: high word of sqrt(1/2)
+    const double m = __hiloint2double(hi - (e << 20), lo);
+    const double f = m - 1.0;
+    const double s = f * rcp_fast(2.0 + f);
+    const double z = s * s;
+    const double z2 = z * z;
+    // Estrin: shorter dependency chain than Horner (DFMA latency 8.3 cycles)
+    const double p01 = fma(kFast[KC_LOG2], z, kFast[KC_LOG1]);
+    const double p23 = fma(kFast[KC_LOG4], z, kFast[KC_LOG3]);
+    const double p45 = fma(kFast[KC_LOG6], z, kFast[KC_LOG5]);
+    const double p47 = fma(kFast[KC_LOG7], z2, p45);
+    const double p03 = fma(p23, z2, p01);
+    const double p = fma(p47, z2 * z2, p03);
+    const double corr = s * fma(-z, p, f);  // s (f - T)
+    const double ed = (double)e;
+    return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
+}
+
 struct LogFrac {
     double num, den;  // <a,b>_log = num / den
 };
@@ -29,10 +79,10 @@ __device__ __forceinline__ LogFrac logfrac(double a, double b, double dl)
 {
     const double d = b - a;
     const double s = b + a;
-    const bool series = d * d < SERIES_EPSILON * (s * s);
+    const bool series = fabs(d) < kFast[KC_SERIES_SQRT] * s;  // s > 0
     const double t = d * rcp_nr1(s);
     const double u = t * t;
-    const double poly = fma(u, fma(u, fma(u, 2.0 / 7.0, 2.0 / 5.0), 2.0 / 3.0), 2.0);
+    const double poly = fma(u, fma(u, fma(u, kFast[KC_LM7], kFast[KC_LM5]), kFast[KC_LM3]), 2.0);
     LogFrac r;
     r.num = series ? s : d;
     r.den = series ? poly : dl;
@@ -78,8 +128,8 @@ __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D,
         dl1 = r.x[0] - l.x[0];
         dl2 = (r.x[0] + l.x[1]) - (l.x[0] + r.x[1]);
     } else {
-        dl1 = log(r.rho * rcp_fast(l.rho));
-        dl2 = log(B * rcp_fast(A));
+        dl1 = log_fast(r.rho * rcp_fast(l.rho));
+        dl2 = log_fast(B * rcp_fast(A));
     }
     const LogFrac m1 = logfrac(l.rho, r.rho, dl1);  // <rho>_log = num1/den1
     const LogFrac m2 = logfrac(A, B, dl2);          // <rho p>_log = 2 num2/den2
@@ -118,8 +168,8 @@ __device__ __forceinline__ void fast_ranocha_w(const Node<D, NX>* const (&L)[W],
             dl1[w] = R[w]->x[0] - L[w]->x[0];
             dl2[w] = (R[w]->x[0] + L[w]->x[1]) - (L[w]->x[0] + R[w]->x[1]);
         } else {
-            dl1[w] = log(R[w]->rho * rcp_fast(L[w]->rho));
-            dl2[w] = log(B[w] * rcp_fast(A[w]));
+            dl1[w] = log_fast(R[w]->rho * rcp_fast(L[w]->rho));
+            dl2[w] = log_fast(B[w] * rcp_fast(A[w]));
         }
     }
     LogFrac m1[W], m2[W];
@@ -190,8 +240,8 @@ __device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const N
         dl1 = r.x[1] - l.x[1];
         dl2 = r.x[2] - l.x[2];
     } else {
-        dl1 = log(r.rho * rcp_fast(l.rho));
-        dl2 = log(r.x[0] * rcp_fast(l.x[0]));
+        dl1 = log_fast(r.rho * rcp_fast(l.rho));
+        dl2 = log_fast(r.x[0] * rcp_fast(l.x[0]));
     }
     const LogFrac m1 = logfrac(l.rho, r.rho, dl1);     // <rho>_log
     const LogFrac m2 = logfrac(l.x[0], r.x[0], dl2);   // <beta>_log
@@ -254,13 +304,13 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     // p/2 = (gamma-1)/2 (E - rho |v|^2 / 2) = (gamma-1)/2 (E - 2 rho |v/2|^2)
     q.p = (0.5 * gm1) * fma(-2.0 * rho, s, u[D + 1]);
     if constexpr (VF == F_RANOCHA && LOGS) {
-        q.x[0] = log(rho);
-        q.x[1] = log(2.0 * q.p);
+        q.x[0] = log_fast(rho);
+        q.x[1] = log_fast(2.0 * q.p);
     } else if constexpr (VF == F_CHANDRASHEKAR) {
         q.x[0] = 0.25 * rho * rcp_fast(q.p);  // beta = rho / (2 p)
         if constexpr (LOGS) {
-            q.x[1] = log(rho);
-            q.x[2] = log(q.x[0]);
+            q.x[1] = log_fast(rho);
+            q.x[2] = log_fast(q.x[0]);
         }
     } else if constexpr (VF == F_KG) {
         q.x[0] = u[D + 1] * hri;  // e/2

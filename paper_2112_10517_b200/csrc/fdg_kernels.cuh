@@ -79,7 +79,7 @@ struct KParams {
 #define FDG_LINE_REGS 0
 #endif
 #ifndef FDG_STAGE_UNROLL
-#define FDG_STAGE_UNROLL 2
+#define FDG_STAGE_UNROLL 1
 #endif
 constexpr int kStageUnroll = FDG_STAGE_UNROLL;
 #ifndef FDG_FACE_UNROLL

@@ -21,10 +21,8 @@ nvcc $COMMON -c fdg_capi.cu -o obj_var/capi.o &
 nvcc $COMMON -c fdg_probe.cu -o obj_var/probe.o &
 declare -A FLAGS=(
   [base]=""
-  [mb7]="-DFDG_MIN_BLOCKS=7"
-  [mb8]="-DFDG_MIN_BLOCKS=8"
-  [t32m13]="-DFDG_TARGET_THREADS=32 -DFDG_MIN_BLOCKS=13"
-  [t32m14]="-DFDG_TARGET_THREADS=32 -DFDG_MIN_BLOCKS=14"
+  [su4]="-DFDG_STAGE_UNROLL=4"
+  [su1]="-DFDG_STAGE_UNROLL=1"
 )
 FMAD=--fmad=true; [[ $UNIT == faithful* ]] && FMAD=--fmad=false
 for name in "${!FLAGS[@]}"; do

@@ -266,6 +266,30 @@ def test_gate_names_first_bad_node():
         P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(kernel="batched"))
 
 
+@pytest.mark.parametrize("pre", ["none", "primitives_and_logs"])
+@pytest.mark.parametrize("vf", ["ranocha", "chandrashekar"])
+def test_fast_log_means_over_wide_ranges(vf, pre):
+    """FAST log means (log_fast, series test |d| < 0.01 s) on states spanning
+    12 decades between elements and up to 1e3 contrast inside an element,
+    against the FAITHFUL arithmetic of the oracle: per-element relative
+    max-norm difference <= 1e-12."""
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    setup, u, _ = workloads.build(2, dims=(4, 4, 4))
+    rng = np.random.default_rng(11)
+    ne, nn = u.shape[:2]
+    scale = 10.0 ** rng.uniform(-6, 6, size=(ne, 1))
+    contrast = np.where(rng.random((ne, 1)) < 0.5, 10.0 ** rng.uniform(-1.5, 1.5, size=(ne, nn)),
+                        rng.uniform(0.9999, 1.0001, size=(ne, nn)))  # also the series branch
+    c = scale * contrast
+    u = u * c[..., None]  # velocity unchanged, rho, p scaled
+    got = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=vf, precompute=pre, kernel="batched"))
+    want = oracle.volume(u, setup, vf, pre, variant="cr")
+    err = np.abs(got - want).max(axis=(1, 2)) / np.abs(want).max(axis=(1, 2))
+    assert err.max() <= 1e-12, err.max()
+
+
 @pytest.mark.parametrize("kernel", ["reference", "batched"])
 def test_pinned_pipeline_matches_device_path(kernel):
     """Pinned host state -> chunked H2D / fdg_volume_range / D2H pipeline:
