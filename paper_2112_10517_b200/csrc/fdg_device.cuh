@@ -445,9 +445,9 @@ struct Gas {
 // Volume two-point flux dispatch (compile-time kind).
 template <int D, int VF, int AXIS, int MODE, int LOGS, int NX>
 __device__ __forceinline__ void volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
-                                            const Gas& gas, int pre, double* f)
+                                            const Gas& gas, int pre, double* f, unsigned vm)
 {
-    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS>(l, r, nrm, gas.igm1, f);
+    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS>(l, r, nrm, gas.igm1, f, vm);
     else if constexpr (VF == F_SHIMA) flux_shima<D, AXIS, MODE>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_RANOCHA) flux_ranocha<D, AXIS, MODE, LOGS>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_CENTRAL) flux_central<D, AXIS, MODE>(l, r, nrm, gas.igm1, pre != PRE_NONE, f);
@@ -600,7 +600,8 @@ __device__ __noinline__ void surface_flux(int kind, const double* ul, const doub
     case K: {                                                           \
         const auto l = make_node<D, K, MODE, 0>(ul, gas.gm1);           \
         const auto r = make_node<D, K, MODE, 0>(ur, gas.gm1);           \
-        volume_flux<D, K, -1, MODE, 0>(l, r, nrm, gas, PRE_NONE, f);    \
+        volume_flux<D, K, -1, MODE, 0>(l, r, nrm, gas, PRE_NONE, f,     \
+                                       __activemask());                 \
         return;                                                         \
     }
         FDG_SURF_SYM(F_SHIMA)

@@ -37,6 +37,33 @@ cudaError_t elem_occupancy(int* blocks_per_sm)
     return err;
 }
 
+// Programmatic dependent launch: an element kernel may be scheduled while the
+// previous kernel of the stream drains; it runs its prologue and then waits
+// (griddepcontrol.wait, before any global memory access) for that kernel's
+// completion and memory flush. Hides launch latency and the parameter-bank
+// warm-up behind the previous kernel's tail (kernel-to-kernel in a solver
+// loop or a CUDA graph); the dependency itself is unchanged.
+template <class Kern>
+cudaError_t launch_kernel(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t s, const KParams& p)
+{
+#if FDG_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+#else
+    kern<<<grid, block, smem, s>>>(p);
+    return cudaGetLastError();
+#endif
+}
+
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS>
 cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
 {
@@ -57,12 +84,11 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
     const long long slots = (long long)bps * sm_count;
     if constexpr (twin) {
         if (nb > slots && nb <= (long long)bps_hi * sm_count) {
-            elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC><<<(unsigned)nb, G::NT, smem, s>>>(p);
-            return cudaGetLastError();
+            return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>, (unsigned)nb, G::NT, smem, s, p);
         }
     }
-    elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0><<<(unsigned)std::min(nb, slots), G::NT, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0>, (unsigned)std::min(nb, slots), G::NT, smem, s,
+                         p);
 }
 
 template <int D, int P1, int VF, bool CURVED, int MODE>

@@ -6,14 +6,21 @@
 //     ph = p/2; exact power-of-two scalings), so every arithmetic mean
 //     {a} = (a_l + a_r)/2 is a single add and the 1/2 factors of the fluxes
 //     fold away;
-//   * the log-mean branch test u < 1e-4 is d^2 < 1e-4 s^2 with d = b - a,
-//     s = b + a (no division); u itself (needed only in the series branch,
-//     where it is < 1e-4) uses an approximate reciprocal with one Newton step;
+//   * the log-mean branch test u < 1e-4 (means.py: u = ((b-a)/(b+a))^2) is
+//     the equivalent |log b - log a| < 2 atanh(0.01) on the log difference
+//     the log branch needs anyway (one compare, no division);
+//   * the series branch can be made WARP-UNIFORM (FDG_SERIES_VOTE=1: its ~20
+//     FP64 instructions per pair run only when a lane of the warp needs
+//     them). Measured on B200 (profiles/r01_tuning.md): +1% on the smooth
+//     64^3 density wave, -5% on cfg5 (59% series pairs) and on precompute
+//     "none" -- the branch stops ptxas from interleaving consecutive pairs --
+//     so the default evaluates both branches and selects;
 //   * <x>_log = num/den with (num, den) = (s, P(u)) or (d, log b - log a); the
 //     two log means of a Ranocha pair share ONE reciprocal 1/(den_rho num_rhop)
 //     (MUFU.RCP64H + two Newton steps, branch free);
-//   * both branches are evaluated and selected (branch fractions mix inside
-//     every warp).
+//   * Ranocha nodes carry log rho and X = log(rho/p): the (rho p) log mean of
+//     (rho_l p_r, rho_r p_l) needs log B - log A = X_r - X_l (one add), and X
+//     reuses the staging reciprocal of rho.
 // Results agree with the reference to a few ulps of each flux (VOL-level
 // relative differences ~1e-15, tests/test_gpu_parity.py).
 #pragma once
@@ -28,7 +35,7 @@ enum FastConst {
     KC_LOG1, KC_LOG2, KC_LOG3, KC_LOG4, KC_LOG5, KC_LOG6, KC_LOG7,  // log_fast T(z) coefficients
     KC_LN2_HI, KC_LN2_LO,
     KC_LM3, KC_LM5, KC_LM7,  // log-mean series 2/3, 2/5, 2/7 (means.py:16-40)
-    KC_SERIES_SQRT,          // sqrt(SERIES_EPSILON): u < 1e-4  <=>  |d| < 0.01 s
+    KC_SERIES_DL,            // u < 1e-4  <=>  |t| < 0.01  <=>  |log(b/a)| < 2 atanh(0.01)
     KC_COUNT
 };
 static __constant__ double kFast[KC_COUNT] = {
@@ -36,7 +43,7 @@ static __constant__ double kFast[KC_COUNT] = {
     0.1818356087762256, 0.15314136991810745, 0.14795104806627174,
     0.6931471805599453, 2.3190468138462996e-17,
     2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0,
-    0.01,
+    0.02000066670666952,
 };
 
 // FAST natural log of a positive normal double, ~1.2 ulp (libdevice's log
@@ -70,23 +77,43 @@ __device__ __forceinline__ double log_fast(double x)
     return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
 }
 
-struct LogFrac {
-    double num, den;  // <a,b>_log = num / den
-};
+#ifndef FDG_SERIES_VOTE
+#define FDG_SERIES_VOTE 0  // 1: warp-uniform series branch (see the header)
+#endif
 
-// log mean of (a, b) as a fraction; dl = log b - log a (only used off the series branch)
-__device__ __forceinline__ LogFrac logfrac(double a, double b, double dl)
+// log-mean branch test on the log difference dl = log b - log a (means.py:
+// u < 1e-4); dl is exact up to the rounding of the two logs
+__device__ __forceinline__ bool series_test(double dl) { return fabs(dl) < kFast[KC_SERIES_DL]; }
+
+// <a,b>_log = num / den: the log branch (num, den) = (b - a, dl) is the
+// caller's; on series lanes replace it by (a + b, 2 + u (2/3 + u (2/5 + u 2/7)))
+__device__ __forceinline__ void series_frac(double a, double b, bool series, double& num, double& den)
 {
-    const double d = b - a;
     const double s = b + a;
-    const bool series = fabs(d) < kFast[KC_SERIES_SQRT] * s;  // s > 0
-    const double t = d * rcp_nr1(s);
+    const double t = num * rcp_nr1(s);  // num = b - a
     const double u = t * t;
     const double poly = fma(u, fma(u, fma(u, kFast[KC_LM7], kFast[KC_LM5]), kFast[KC_LM3]), 2.0);
-    LogFrac r;
-    r.num = series ? s : d;
-    r.den = series ? poly : dl;
-    return r;
+    num = series ? s : num;
+    den = series ? poly : den;
+}
+
+// both log means of a pair; the series work only when a lane of the warp needs it
+__device__ __forceinline__ void logmean_pair(double a1, double b1, double dl1, double& num1, double& den1, double a2,
+                                             double b2, double dl2, double& num2, double& den2, unsigned vm)
+{
+    num1 = b1 - a1;
+    den1 = dl1;
+    num2 = b2 - a2;
+    den2 = dl2;
+    const bool s1 = series_test(dl1);
+    const bool s2 = series_test(dl2);
+#if FDG_SERIES_VOTE
+    if (__any_sync(vm, s1 || s2))
+#endif
+    {
+        series_frac(a1, b1, s1, num1, den1);
+        series_frac(a2, b2, s2, num2, den2);
+    }
 }
 
 // half-value dot products with the face/metric direction
@@ -118,25 +145,25 @@ __device__ __forceinline__ void fast_momentum(double f_rho, double p_avg, const 
 
 template <int D, int AXIS, int LOGS, int NX>
 __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
-                                             double igm1, double* f)
+                                             double igm1, double* f, unsigned vm)
 {
     // rho-mean and the (rho p)-mean; A = rho_l p_r / 2, B = rho_r p_l / 2
     const double A = l.rho * r.p;
     const double B = r.rho * l.p;
     double dl1, dl2;
     if constexpr (LOGS) {
-        dl1 = r.x[0] - l.x[0];
-        dl2 = (r.x[0] + l.x[1]) - (l.x[0] + r.x[1]);
+        dl1 = r.x[0] - l.x[0];  // log rho_r - log rho_l
+        dl2 = r.x[1] - l.x[1];  // log B - log A = X_r - X_l, X = log(rho/p)
     } else {
         dl1 = log_fast(r.rho * rcp_fast(l.rho));
         dl2 = log_fast(B * rcp_fast(A));
     }
-    const LogFrac m1 = logfrac(l.rho, r.rho, dl1);  // <rho>_log = num1/den1
-    const LogFrac m2 = logfrac(A, B, dl2);          // <rho p>_log = 2 num2/den2
-    const double rr = rcp_fast(m1.den * m2.num);
-    const double rho_mean = m1.num * m2.num * rr;
+    double num1, den1, num2, den2;  // <rho>_log = num1/den1, <rho p>_log = 2 num2/den2
+    logmean_pair(l.rho, r.rho, dl1, num1, den1, A, B, dl2, num2, den2, vm);
+    const double rr = rcp_fast(den1 * num2);
+    const double rho_mean = num1 * num2 * rr;
     // igm1 p_l p_r / <rho p>_log = igm1 (4 ph_l ph_r) den2 / (2 num2)
-    const double e_int = (2.0 * igm1) * (l.p * r.p) * (m1.den * m2.den) * rr;
+    const double e_int = (2.0 * igm1) * (l.p * r.p) * (den1 * den2) * rr;
     const double vn_l = hdot<D, AXIS>(l.v, nrm);
     const double vn_r = hdot<D, AXIS>(r.v, nrm);
     const double f_rho = rho_mean * (vn_l + vn_r);
@@ -148,55 +175,6 @@ __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D,
     f[0] = f_rho;
     f[D + 1] = fma(f_rho, fma(2.0, vv, e_int), 2.0 * pv);
     fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
-}
-
-// W independent Ranocha pairs evaluated statement by statement side by side:
-// the FP64 pipe needs ~4 independent instructions in flight per scheduler
-// (DFMA latency 8.3 cycles, one warp-DFMA issued per 2 cycles, measured by
-// scripts/micro/fp64_latency.cu); one pair's dependency chain is ~25 deep,
-// so interleaving W pairs multiplies the available ILP by W.
-template <int D, int AXIS, int LOGS, int NX, int W>
-__device__ __forceinline__ void fast_ranocha_w(const Node<D, NX>* const (&L)[W], const Node<D, NX>* const (&R)[W],
-                                               const double (&nrm)[W][D], double igm1, double (&f)[W][D + 2])
-{
-    double A[W], B[W], dl1[W], dl2[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        A[w] = L[w]->rho * R[w]->p;
-        B[w] = R[w]->rho * L[w]->p;
-        if constexpr (LOGS) {
-            dl1[w] = R[w]->x[0] - L[w]->x[0];
-            dl2[w] = (R[w]->x[0] + L[w]->x[1]) - (L[w]->x[0] + R[w]->x[1]);
-        } else {
-            dl1[w] = log_fast(R[w]->rho * rcp_fast(L[w]->rho));
-            dl2[w] = log_fast(B[w] * rcp_fast(A[w]));
-        }
-    }
-    LogFrac m1[W], m2[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) m1[w] = logfrac(L[w]->rho, R[w]->rho, dl1[w]);
-#pragma unroll
-    for (int w = 0; w < W; ++w) m2[w] = logfrac(A[w], B[w], dl2[w]);
-    double rr[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) rr[w] = rcp_fast(m1[w].den * m2[w].num);
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const Node<D, NX>& l = *L[w];
-        const Node<D, NX>& r = *R[w];
-        const double rho_mean = m1[w].num * m2[w].num * rr[w];
-        const double e_int = (2.0 * igm1) * (l.p * r.p) * (m1[w].den * m2[w].den) * rr[w];
-        const double vn_l = hdot<D, AXIS>(l.v, nrm[w]);
-        const double vn_r = hdot<D, AXIS>(r.v, nrm[w]);
-        const double f_rho = rho_mean * (vn_l + vn_r);
-        double vv = l.v[0] * r.v[0];
-#pragma unroll
-        for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
-        const double pv = fma(l.p, vn_r, r.p * vn_l);
-        f[w][0] = f_rho;
-        f[w][D + 1] = fma(f_rho, fma(2.0, vv, e_int), 2.0 * pv);
-        fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm[w], f[w]);
-    }
 }
 
 template <int D, int AXIS, int NX>
@@ -233,7 +211,7 @@ __device__ __forceinline__ void fast_kg(const Node<D, NX>& l, const Node<D, NX>&
 // Chandrashekar; x[0] = beta = rho/(2p), x[1] = log rho, x[2] = log beta (LOGS)
 template <int D, int AXIS, int LOGS, int NX>
 __device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
-                                                   double igm1, double* f)
+                                                   double igm1, double* f, unsigned vm)
 {
     double dl1, dl2;
     if constexpr (LOGS) {
@@ -243,13 +221,13 @@ __device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const N
         dl1 = log_fast(r.rho * rcp_fast(l.rho));
         dl2 = log_fast(r.x[0] * rcp_fast(l.x[0]));
     }
-    const LogFrac m1 = logfrac(l.rho, r.rho, dl1);     // <rho>_log
-    const LogFrac m2 = logfrac(l.x[0], r.x[0], dl2);   // <beta>_log
+    double num1, den1, num2, den2;  // <rho>_log = num1/den1, <beta>_log = num2/den2
+    logmean_pair(l.rho, r.rho, dl1, num1, den1, l.x[0], r.x[0], dl2, num2, den2, vm);
     const double bsum = l.x[0] + r.x[0];               // 2 {beta}
-    const double rr = rcp_fast(m1.den * m2.num * bsum);
-    const double rho_mean = m1.num * m2.num * bsum * rr;
-    const double inv_beta_mean = m2.den * m1.den * bsum * rr;
-    const double p_tilde = 0.5 * (l.rho + r.rho) * (m1.den * m2.num) * rr;  // {rho} / (2 {beta})
+    const double rr = rcp_fast(den1 * num2 * bsum);
+    const double rho_mean = num1 * num2 * bsum * rr;
+    const double inv_beta_mean = den2 * den1 * bsum * rr;
+    const double p_tilde = 0.5 * (l.rho + r.rho) * (den1 * num2) * rr;  // {rho} / (2 {beta})
     const double vn_avg = hdot<D, AXIS>(l.v, nrm) + hdot<D, AXIS>(r.v, nrm);
     const double f_rho = rho_mean * vn_avg;
     double v2 = 0.0;  // {|v|^2}/2 = |vh_l|^2 + |vh_r|^2
@@ -305,7 +283,7 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     q.p = (0.5 * gm1) * fma(-2.0 * rho, s, u[D + 1]);
     if constexpr (VF == F_RANOCHA && LOGS) {
         q.x[0] = log_fast(rho);
-        q.x[1] = log_fast(2.0 * q.p);
+        q.x[1] = -log_fast(4.0 * q.p * hri);  // X = log(rho / p) = -log(2 ph / rho), 2 hri = 1/rho
     } else if constexpr (VF == F_CHANDRASHEKAR) {
         q.x[0] = 0.25 * rho * rcp_fast(q.p);  // beta = rho / (2 p)
         if constexpr (LOGS) {
@@ -321,15 +299,16 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     return q;
 }
 
+// vm: lanes of the warp executing this call together (the series-branch vote)
 template <int D, int VF, int AXIS, int LOGS, int NX>
 __device__ __forceinline__ void fast_volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
-                                                 double igm1, double* f)
+                                                 double igm1, double* f, unsigned vm)
 {
     if constexpr (VF == F_SHIMA) fast_shima<D, AXIS>(l, r, nrm, igm1, f);
-    else if constexpr (VF == F_RANOCHA) fast_ranocha<D, AXIS, LOGS>(l, r, nrm, igm1, f);
+    else if constexpr (VF == F_RANOCHA) fast_ranocha<D, AXIS, LOGS>(l, r, nrm, igm1, f, vm);
     else if constexpr (VF == F_CENTRAL) fast_central<D, AXIS>(l, r, nrm, f);
     else if constexpr (VF == F_KG) fast_kg<D, AXIS>(l, r, nrm, f);
-    else fast_chandrashekar<D, AXIS, LOGS>(l, r, nrm, igm1, f);
+    else fast_chandrashekar<D, AXIS, LOGS>(l, r, nrm, igm1, f, vm);
 }
 
 }  // namespace fdg

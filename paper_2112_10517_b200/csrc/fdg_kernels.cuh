@@ -92,13 +92,22 @@ constexpr int kFaceUnroll = FDG_FACE_UNROLL;
 #ifndef FDG_PREFETCH
 #define FDG_PREFETCH 1
 #endif
-
+#ifndef FDG_PDL
+#define FDG_PDL 0  // 1: programmatic dependent launch (fdg_dispatch.cuh); measured no gain in a CUDA graph
+#endif
 template <int D, int P1>
 struct Geo {
     static constexpr int NN = ipow(P1, D);
     static constexpr int LINES = ipow(P1, D - 1);
     static constexpr int NVAR = D + 2;
-    static constexpr int NNP = NN + FDG_PAD * (NN / P1);  // one pad slot per innermost row
+    // 3D, p + 1 = 4: nodes XOR-swizzled instead of padded (SWZ): with a
+    // half-warp on 16 lines at one line position (any direction) every bank
+    // pair is hit exactly once, and the element block stays 64 slots
+#ifndef FDG_SWIZZLE
+#define FDG_SWIZZLE 1
+#endif
+    static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && P1 == 4;
+    static constexpr int NNP = SWZ ? NN : NN + FDG_PAD * (NN / P1);  // else one pad slot per innermost row
     static constexpr int EPB = LINES >= FDG_TARGET_THREADS ? 1 : FDG_TARGET_THREADS / LINES;
     // resident-CTA hint for __launch_bounds__ (register cap 64K / (NT * MINB))
     static constexpr int MINB = FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (P1 <= 5 ? 6 : 1);
@@ -116,7 +125,11 @@ struct Geo {
         constexpr int stride = ipow(P1, D - 1 - N);
         return (m / stride * P1 + a) * stride + m % stride;
     }
-    __device__ static __forceinline__ int pad(int node) { return FDG_PAD ? node + node / P1 : node; }
+    __device__ static __forceinline__ int pad(int node)
+    {
+        if constexpr (SWZ) return node ^ (((node >> 4) * 5) & 15);  // bank pair (node & 15) ^ 5 (node >> 4)
+        else return FDG_PAD ? node + node / P1 : node;
+    }
     // accumulator slot of (variable v, element el, node)
     __device__ static __forceinline__ int acc(int v, int el, int node) { return v * FA + el * NNP + pad(node); }
 };
@@ -174,81 +187,10 @@ __device__ __forceinline__ Node<D, NX> load_node(const double* sq, int fs, int i
     return q;
 }
 
-// Round-robin (circle method) order of the p(p+1)/2 pairs of a line: every
-// round is a set of disjoint pairs, so consecutive pairs update different
-// accumulators (FAST mode; FAITHFUL keeps the pair-table order).
-template <int P1>
-struct Tour {
-    static constexpr int NP = P1 * (P1 - 1) / 2;
-    int a[NP > 0 ? NP : 1], b[NP > 0 ? NP : 1];
-};
-
-template <int P1>
-__host__ __device__ constexpr Tour<P1> tournament()
-{
-    Tour<P1> t{};
-    const int n = P1 + (P1 % 2);  // even number of slots (one dummy if P1 is odd)
-    int k = 0;
-    for (int r = 0; r < n - 1; ++r) {
-        for (int i = 0; i < n / 2; ++i) {
-            int x = (i == 0) ? n - 1 : (r + i) % (n - 1);
-            int y = (i == 0) ? r : (r - i + (n - 1)) % (n - 1);
-            if (x >= P1 || y >= P1) continue;  // the dummy's pairing: a bye
-            t.a[k] = x < y ? x : y;
-            t.b[k] = x < y ? y : x;
-            ++k;
-        }
-    }
-    return t;
-}
-
-#ifndef FDG_WIDE
-#define FDG_WIDE 1  // measured: no gain over the compiler's own interleaving (W = 2, 3, 6)
-#endif
-
-// FAST Ranocha, W pairs side by side in round-robin order (line data in registers)
-template <int D, int P1, bool CURVED, int LOGS, int N, int NX>
-__device__ __forceinline__ void volume_pairs_wide(const KParams& prm, const Node<D, NX> (&q)[P1],
-                                                  const double (&jl)[CURVED ? P1 : 1][D],
-                                                  double (&acc)[P1][D + 2])
-{
-    constexpr Tour<P1> T = tournament<P1>();
-    constexpr int NP = Tour<P1>::NP;
-    constexpr int W = FDG_WIDE;
-    sfor<0, (NP + W - 1) / W>([&](auto C) {
-        constexpr int k0 = decltype(C)::value * W;
-        constexpr int WE = (NP - k0) < W ? (NP - k0) : W;
-        const Node<D, NX>* L[WE];
-        const Node<D, NX>* R[WE];
-        double nrm[WE][D];
-        double f[WE][D + 2];
-        sfor<0, WE>([&](auto I) {
-            constexpr int w = decltype(I)::value;
-            constexpr int a = T.a[k0 + w], b = T.b[k0 + w];
-            L[w] = &q[a];
-            R[w] = &q[b];
-#pragma unroll
-            for (int j = 0; j < D; ++j) nrm[w][j] = CURVED ? 0.5 * (jl[CURVED ? a : 0][j] + jl[CURVED ? b : 0][j]) : 0.0;
-        });
-        fast_ranocha_w<D, CURVED ? -1 : N, LOGS, NX, WE>(L, R, nrm, prm.gas.igm1, f);
-        sfor<0, WE>([&](auto I) {
-            constexpr int w = decltype(I)::value;
-            constexpr int a = T.a[k0 + w], b = T.b[k0 + w];
-            const double wa = prm.wts[N][a * P1 + b];
-            const double wb = prm.wts[N][b * P1 + a];
-#pragma unroll
-            for (int v = 0; v < D + 2; ++v) {
-                acc[a][v] = fma(wa, f[w][v], acc[a][v]);
-                acc[b][v] = fma(wb, f[w][v], acc[b][v]);
-            }
-        });
-    });
-}
-
 // One direction of the volume integral for the thread's line.
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
 __device__ __forceinline__ void volume_direction(const KParams& prm, const double* sq, double* sacc, int el,
-                                                 int m, long long e)
+                                                 int m, long long e, unsigned vm)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
@@ -276,19 +218,6 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
             for (int j = 0; j < D; ++j) jl[a][j] = __ldg(prm.ja + ((e * G::NN + nodes[a]) * D + N) * D + j);
     }
     const int sbase = el * G::NNP;
-    if constexpr (MODE == FAST && VF == F_RANOCHA && FDG_WIDE > 1) {
-        Node<D, NX> ql[P1];
-        sfor<0, P1>([&](auto A) {
-            constexpr int a = decltype(A)::value;
-            ql[a] = load_node<D, NX>(sq, G::FS, sbase + G::pad(nodes[a]));
-        });
-        volume_pairs_wide<D, P1, CURVED, LOGS, N>(prm, ql, jl, acc);
-#pragma unroll
-        for (int a = 0; a < P1; ++a)
-#pragma unroll
-            for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, nodes[a])] = acc[a][v];
-        return;
-    }
 #if FDG_LINE_REGS
     // the whole line's node data in registers: P1 shared-memory loads per node
     // instead of one per pair it takes part in
@@ -322,9 +251,9 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
                 double alpha[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) alpha[j] = 0.5 * (jl[a][j] + jl[b][j]);
-                volume_flux<D, VF, -1, MODE, LOGS>(qa, qb, alpha, prm.gas, prm.precompute, f);
+                volume_flux<D, VF, -1, MODE, LOGS>(qa, qb, alpha, prm.gas, prm.precompute, f, vm);
             } else {
-                volume_flux<D, VF, N, MODE, LOGS>(qa, qb, nullptr, prm.gas, prm.precompute, f);
+                volume_flux<D, VF, N, MODE, LOGS>(qa, qb, nullptr, prm.gas, prm.precompute, f, vm);
             }
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) {
@@ -337,6 +266,17 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
     for (int a = 0; a < P1; ++a)
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, nodes[a])] = acc[a][v];
+}
+
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
+__device__ __forceinline__ void vdir(const KParams& prm, const double* sq, double* sacc, int el, int m, long long e,
+                                     bool active, unsigned vm)
+{
+    if constexpr (MODE == FAST) {
+        if (vm) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N>(prm, sq, sacc, el, m, active ? e : e - el, vm);
+    } else {
+        if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N>(prm, sq, sacc, el, m, e, 0u);
+    }
 }
 
 template <int D>
@@ -469,6 +409,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
     double* sq = smem;                        // (2+D+NX) fields x FS
     double* sacc = smem + sq_doubles<D, P1, VF, LOGS>();  // NVAR x FA (AoS u staging before the volume pass)
     const int tid = threadIdx.x;
+#if FDG_PDL
+    // launched with programmatic stream serialization (fdg_dispatch.cuh):
+    // everything above touches only registers and the parameter bank
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 #if FDG_PHASE_TIMING
     long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long pt_last_ = clock64();
@@ -477,6 +423,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
 #endif
     const int el = tid / G::LINES;
     const int m = tid % G::LINES;
+    // lanes holding a line of the batch: the FAST volume phases run on all of
+    // them (lanes of absent elements in a ragged last batch compute on stale
+    // shared data that is never stored), so the series-branch vote sees whole
+    // warps -- a compile-time full mask when the CTA has no spare threads
+    constexpr int USED = EPB * G::LINES;
+    const unsigned vmask = (USED == NT) ? 0xffffffffu : __ballot_sync(0xffffffffu, tid < USED) * (tid < USED);
     const long long nbatch = (prm.n_elem + EPB - 1) / EPB;
     const int epi = prm.epilogue;
 
@@ -550,14 +502,14 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
             __syncthreads();
             FDG_PT(1)
             // ---- volume integral, direction by direction (accumulators: SoA)
-            if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e);
+            vdir<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e, active, vmask);
             __syncthreads();
             FDG_PT(2)
-            if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e);
+            vdir<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e, active, vmask);
             __syncthreads();
             FDG_PT(3)
             if constexpr (D == 3) {
-                if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e);
+                vdir<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e, active, vmask);
                 __syncthreads();
             }
             FDG_PT(4)

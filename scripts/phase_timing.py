@@ -28,7 +28,7 @@ for dims in [(16, 16, 16), (64, 64, 64)]:
     torch.cuda.synchronize()
     L.fdg_debug_phase_cycles(buf, 1)
     tot = sum(buf)
-    batches = 5 * (setup.n_elements // 8)
+    batches = 5 * (setup.n_elements // 4)  # EPB = 4 (64-thread CTAs at N = 3)
     print(dims, "cycles per batch per CTA:", {n: round(buf[i] / batches) for i, n in enumerate(names) if buf[i]},
           "total", round(tot / batches))
 
