@@ -9,13 +9,13 @@
 //   * the log-mean branch test u < 1e-4 (means.py: u = ((b-a)/(b+a))^2) is
 //     the equivalent |log b - log a| < 2 atanh(0.01) on the log difference
 //     the log branch needs anyway (one compare, no division);
-//   * the series branch can be made WARP-UNIFORM (FDG_SERIES_VOTE=1: its ~20
-//     FP64 instructions per pair run only when a lane of the warp needs
-//     them). Measured on B200 (profiles/r01_tuning.md): +1% on the smooth
-//     64^3 density wave, -5% on cfg5 (59% series pairs) and on precompute
-//     "none" -- the branch stops ptxas from interleaving consecutive pairs --
-//     so the default evaluates both branches and selects;
-//   * <x>_log = num/den with (num, den) = (s, P(u)) or (d, log b - log a); the
+//   * the series branch is (a+b)/(2 x coth x), x = (log b - log a)/2, a
+//     polynomial in (log b - log a)^2 (series_frac): no reciprocal, and
+//     both branches are evaluated and selected (branch fractions mix inside
+//     every warp; a warp-uniform series branch,
+//     FDG_SERIES_VOTE=1, measured slower: it stops ptxas from interleaving
+//     consecutive pairs, profiles/r01_tuning.md);
+//   * <x>_log = num/den with (num, den) = (a+b, 2x coth x) or (b-a, dl); the
 //     two log means of a Ranocha pair share ONE reciprocal 1/(den_rho num_rhop)
 //     (MUFU.RCP64H + two Newton steps, branch free);
 //   * Ranocha nodes carry log rho and X = log(rho/p): the (rho p) log mean of
@@ -34,7 +34,7 @@ namespace fdg {
 enum FastConst {
     KC_LOG1, KC_LOG2, KC_LOG3, KC_LOG4, KC_LOG5, KC_LOG6, KC_LOG7,  // log_fast T(z) coefficients
     KC_LN2_HI, KC_LN2_LO,
-    KC_LM3, KC_LM5, KC_LM7,  // log-mean series 2/3, 2/5, 2/7 (means.py:16-40)
+    KC_CT1, KC_CT2, KC_CT3,  // 2 x coth x = 2 + z/6 - z^2/360 + z^3/15120, z = (2x)^2
     KC_SERIES_DL,            // u < 1e-4  <=>  |t| < 0.01  <=>  |log(b/a)| < 2 atanh(0.01)
     KC_COUNT
 };
@@ -42,23 +42,26 @@ static __constant__ double kFast[KC_COUNT] = {
     0.6666666666666734, 0.39999999999417485, 0.2857142874173421, 0.22222198640440488,
     0.1818356087762256, 0.15314136991810745, 0.14795104806627174,
     0.6931471805599453, 2.3190468138462996e-17,
-    2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0,
+    1.0 / 6.0, -1.0 / 360.0, 1.0 / 15120.0,
     0.02000066670666952,
 };
 
-// FAST natural log of a positive normal double, ~1.2 ulp (libdevice's log
-// costs ~86 instructions per call here, 20% of the cfg2 kernel; this one ~28).
+// FAST natural log, ~1.2 ulp (libdevice's log costs ~86 instructions per
+// call here, 20% of the cfg2 kernel before this one; this is ~28).
 // x = 2^e m, m in [sqrt(1/2), sqrt(2)); log m = f - s (f - T(z)), f = m - 1
 // (exact), s = f / (2 + f), z = s^2, T(z) = 2 (atanh(s)/s - 1) fitted to
 // degree 7 (scripts/gen_logfast.py: coefficients and the error check).
-// Zero, negative, subnormal, inf and NaN arguments take libdevice's log.
-static __device__ __noinline__ double log_slow(double x) { return log(x); }
-
+// Branch free (a call or branch for special inputs would keep ptxas from
+// interleaving the logs of consecutive nodes): subnormals are rescaled by
+// 2^54, and zero / negative / inf / NaN arguments select -inf / NaN / inf /
+// NaN at the end.
 __device__ __forceinline__ double log_fast(double x)
 {
-    const int hi = __double2hiint(x);
-    const int lo = __double2loint(x);
-    if (hi < 0x00100000 || hi >= 0x7ff00000) return log_slow(x);  // out of line: keeps the pair loops small
+    const long long bits = __double_as_longlong(x);
+    const bool sub = bits < 0x0010000000000000LL;  // subnormal, zero or negative
+    const double xs = sub ? x * 0x1p54 : x;
+    const int hi = __double2hiint(xs);
+    const int lo = __double2loint(xs);
     const int e = (hi - 0x3fe6a09e) >> 20;  // 0x3fe6a09e: high word of sqrt(1/2)
     const double m = __hiloint2double(hi - (e << 20), lo);
     const double f = m - 1.0;
@@ -73,8 +76,12 @@ __device__ __forceinline__ double log_fast(double x)
     const double p03 = fma(p23, z2, p01);
     const double p = fma(p47, z2 * z2, p03);
     const double corr = s * fma(-z, p, f);  // s (f - T)
-    const double ed = (double)e;
-    return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
+    const double ed = (double)(sub ? e - 54 : e);
+    const double r = fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
+    const bool ok = bits > 0 && bits < 0x7ff0000000000000LL;  // positive, finite
+    const double special = (bits == 0 || bits == (long long)0x8000000000000000ULL) ? -INFINITY
+                           : (bits < 0) ? NAN : x;  // -0, +0 | negative | +inf, NaN
+    return ok ? r : special;
 }
 
 #ifndef FDG_SERIES_VOTE
@@ -86,15 +93,19 @@ __device__ __forceinline__ double log_fast(double x)
 __device__ __forceinline__ bool series_test(double dl) { return fabs(dl) < kFast[KC_SERIES_DL]; }
 
 // <a,b>_log = num / den: the log branch (num, den) = (b - a, dl) is the
-// caller's; on series lanes replace it by (a + b, 2 + u (2/3 + u (2/5 + u 2/7)))
-__device__ __forceinline__ void series_frac(double a, double b, bool series, double& num, double& den)
+// caller's; on series lanes it becomes (a + b, 2 x coth x), x = dl/2.
+// With t = (b-a)/(b+a) = tanh(x), <a,b>_log = (b-a)/dl = (a+b) tanh(x)/(2x)
+// exactly; means.py's series (a+b)/(2 + u (2/3 + ...)), u = t^2, is the same
+// function of t.  2 x coth x = 2 + z/6 - z^2/360 + z^3/15120 - ..., z = dl^2:
+// dl enters only through the O(z) corrections, so its rounding (which is why
+// (b-a)/dl fails for b ~ a) costs nothing, and no reciprocal is needed
+// (truncation < 1e-19 relative for |dl| < 0.02).
+__device__ __forceinline__ void series_frac(double a, double b, double dl, bool series, double& num, double& den)
 {
-    const double s = b + a;
-    const double t = num * rcp_nr1(s);  // num = b - a
-    const double u = t * t;
-    const double poly = fma(u, fma(u, fma(u, kFast[KC_LM7], kFast[KC_LM5]), kFast[KC_LM3]), 2.0);
-    num = series ? s : num;
-    den = series ? poly : den;
+    const double z = dl * dl;
+    const double cth = fma(z, fma(z, fma(z, kFast[KC_CT3], kFast[KC_CT2]), kFast[KC_CT1]), 2.0);
+    num = series ? b + a : num;
+    den = series ? cth : den;
 }
 
 // both log means of a pair; the series work only when a lane of the warp needs it
@@ -111,8 +122,8 @@ __device__ __forceinline__ void logmean_pair(double a1, double b1, double dl1, d
     if (__any_sync(vm, s1 || s2))
 #endif
     {
-        series_frac(a1, b1, s1, num1, den1);
-        series_frac(a2, b2, s2, num2, den2);
+        series_frac(a1, b1, dl1, s1, num1, den1);
+        series_frac(a2, b2, dl2, s2, num2, den2);
     }
 }
 
@@ -160,20 +171,23 @@ __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D,
     }
     double num1, den1, num2, den2;  // <rho>_log = num1/den1, <rho p>_log = 2 num2/den2
     logmean_pair(l.rho, r.rho, dl1, num1, den1, A, B, dl2, num2, den2, vm);
-    const double rr = rcp_fast(den1 * num2);
-    const double rho_mean = num1 * num2 * rr;
-    // igm1 p_l p_r / <rho p>_log = igm1 (4 ph_l ph_r) den2 / (2 num2)
-    const double e_int = (2.0 * igm1) * (l.p * r.p) * (den1 * den2) * rr;
+    // everything that does not need the shared reciprocal is formed while
+    // MUFU + its correction run; after it: one multiply (f_rho) and one FMA
+    // (the energy factor) ahead of the flux assembly
     const double vn_l = hdot<D, AXIS>(l.v, nrm);
     const double vn_r = hdot<D, AXIS>(r.v, nrm);
-    const double f_rho = rho_mean * (vn_l + vn_r);
+    const double pre_rho = num1 * num2 * (vn_l + vn_r);              // f_rho / rr
+    const double pre_e = (2.0 * igm1) * (l.p * r.p) * (den1 * den2);  // e_int / rr
     double vv = l.v[0] * r.v[0];
 #pragma unroll
     for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
-    // f_E = f_rho (v_l.v_r / 2 + igm1 p_l p_r/<rho p>) + (p_l vn_r + p_r vn_l)/2
     const double pv = fma(l.p, vn_r, r.p * vn_l);
+    const double rr = rcp_fast(den1 * num2);
+    // <rho>_log {v.n}; igm1 p_l p_r / <rho p>_log = igm1 (4 ph_l ph_r) den2 / (2 num2)
+    const double f_rho = pre_rho * rr;
+    // f_E = f_rho (v_l.v_r / 2 + igm1 p_l p_r/<rho p>) + (p_l vn_r + p_r vn_l)/2
     f[0] = f_rho;
-    f[D + 1] = fma(f_rho, fma(2.0, vv, e_int), 2.0 * pv);
+    f[D + 1] = fma(f_rho, fma(pre_e, rr, 2.0 * vv), 2.0 * pv);
     fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
 }
 

@@ -367,7 +367,7 @@ __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, 
 #if FDG_PHASE_TIMING
 // profiling build only (scripts/variants.sh): SM cycles per phase, summed over CTAs/batches
 __device__ unsigned long long fdg_phase_cycles[8];
-__device__ unsigned long long fdg_cta_ns[2 * 8192];  // per-CTA globaltimer start/end (first launch after reset)
+__device__ unsigned long long fdg_cta_ns[3 * 8192];  // per-CTA globaltimer start/end, SM id
 extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
 {
     cudaDeviceSynchronize();
@@ -381,7 +381,7 @@ extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
 extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, fdg_cta_ns, sizeof(unsigned long long) * 2 * n);
+    cudaMemcpyFromSymbol(out, fdg_cta_ns, sizeof(unsigned long long) * 3 * n);
     return 0;
 }
 #define FDG_PT(i)                          \
@@ -486,18 +486,37 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
             }
             __syncthreads();
             FDG_PT(0)
+            {
+                // the gate's rare paths leave the node loop: its body is
+                // straight-line arithmetic that ptxas can interleave
+                unsigned slow = 0;                     // FAST: nodes needing the reference pressure test
+                unsigned long long bad = ~0ull;        // first failing flat node of this thread
 #pragma unroll(kStageUnroll)
-            for (int k = 0; k < KN; ++k) {
-                const int t = tid + k * NT;
-                if (t < ne * NN) {
-                    const int tel = t / NN, node = t - tel * NN;
-                    const double* su = sacc + t * NVAR;
-                    const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
-                    const bool ok = (MODE == FAST) ? gate_ok_fast<D>(su, 2.0 * q.p, prm.gas.gm1)
-                                                   : gate_ok<D>(su, prm.gas.gm1);
-                    if (!ok) atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN + t));
-                    store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
+                for (int k = 0; k < KN; ++k) {
+                    const int t = tid + k * NT;
+                    if (t < ne * NN) {
+                        const int tel = t / NN, node = t - tel * NN;
+                        const double* su = sacc + t * NVAR;
+                        const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
+                        if constexpr (MODE == FAST) {
+                            const int g = gate_fast<D>(su, 2.0 * q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
+                            slow |= (g < 0) ? (1u << k) : 0u;
+                            bad = (g == 0 && (unsigned long long)t < bad) ? (unsigned long long)t : bad;
+                        } else {
+                            bad = (!gate_ok<D>(su, prm.gas.gm1) && (unsigned long long)t < bad) ? (unsigned long long)t : bad;
+                        }
+                        store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
+                    }
                 }
+                if (slow) {
+#pragma unroll 1
+                    for (int k = 0; k < KN; ++k) {
+                        const int t = tid + k * NT;
+                        if (((slow >> k) & 1u) && !gate_ok<D>(sacc + t * NVAR, prm.gas.gm1) && (unsigned long long)t < bad)
+                            bad = t;
+                    }
+                }
+                if (bad != ~0ull) atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN) + bad);
             }
             __syncthreads();
             FDG_PT(1)
@@ -645,8 +664,11 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
     if (tid == 0 && blockIdx.x < 8192) {
         unsigned long long ns1_;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1_));
-        fdg_cta_ns[2 * blockIdx.x] = ns0_;
-        fdg_cta_ns[2 * blockIdx.x + 1] = ns1_;
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+        fdg_cta_ns[3 * blockIdx.x] = ns0_;
+        fdg_cta_ns[3 * blockIdx.x + 1] = ns1_;
+        fdg_cta_ns[3 * blockIdx.x + 2] = smid_;
     }
 #endif
 }

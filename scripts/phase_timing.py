@@ -47,11 +47,20 @@ flush.sum()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(); dm.volume(u, s, out=out); e1.record(); torch.cuda.synchronize()
 n = 1024
-buf = (ctypes.c_ulonglong * (2 * n))()
+buf = (ctypes.c_ulonglong * (3 * n))()
 L.fdg_debug_cta_ns(buf, n)
 import numpy as np
-a = np.array(buf[:], dtype=np.float64).reshape(n, 2)
+a = np.array(buf[:], dtype=np.float64).reshape(n, 3)
 t0 = a[:, 0].min()
-st, en = a[:, 0] - t0, a[:, 1] - t0
+st, en, sm = a[:, 0] - t0, a[:, 1] - t0, a[:, 2].astype(int)
 print("event ms %.4f | CTA start: min %.0f med %.0f max %.0f ns | end: min %.0f med %.0f max %.0f ns | dur med %.0f max %.0f"
       % (e0.elapsed_time(e1), st.min(), np.median(st), st.max(), en.min(), np.median(en), en.max(), np.median(en - st), (en - st).max()))
+per_sm = np.bincount(sm, minlength=148)
+print("CTAs per SM: histogram", {int(k): int(v) for k, v in zip(*np.unique(per_sm, return_counts=True))})
+sm_end = np.zeros(148)
+for i in range(n):
+    sm_end[sm[i]] = max(sm_end[sm[i]], en[i])
+for c in sorted(set(per_sm)):
+    sel = per_sm == c
+    if sel.any():
+        print("  SMs with %d CTAs: %d, last CTA end med %.0f max %.0f ns" % (c, sel.sum(), np.median(sm_end[sel]), sm_end[sel].max()))
