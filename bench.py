@@ -407,8 +407,11 @@ def main():
     del flush, graph
 
     # ---- end to end through the public API with pinned host buffers
-    u_pin = torch.empty(u_host.shape, dtype=torch.float64, pin_memory=True)
-    u_pin.copy_(torch.from_numpy(u_host))
+    # pinned input filled by pin_memory()'s own copy: a multithreaded torch
+    # copy_ into an existing pinned buffer left its H2D at ~0.38-0.46 ms
+    # instead of 0.20 ms on the same box (scripts/e2e_probe.py,
+    # profiles/r01_e2e.md); the fill is setup, outside the timed region
+    u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
     out_pin = torch.empty(u_host.shape, dtype=torch.float64, pin_memory=True)
     for _ in range(max(args.warmup, 3)):
         mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)

@@ -8,19 +8,20 @@ namespace fdg {
 
 using LaunchFn = cudaError_t (*)(const KParams&, cudaStream_t, int sm_count);
 
-// High-occupancy twin: FAST 3D kernels with P1 <= 5 are also built with an
-// 8-CTA register cap (128 regs at 64 threads). The default (6 CTAs, 168 regs)
-// is 4% faster per element in steady state, but when a launch fits in one wave
-// only at the higher occupancy (cfg2: 1024 batches vs 888 / 1184 slots) the
-// twin removes the second, mostly empty wave: cfg2 VOL 20.4 -> 18.4 us, RHS
-// 51 -> 39 us (profiles/r01_tuning.md).
+// High-occupancy twin: FAST 3D kernels whose default occupancy is below 8
+// CTAs (p+1 = 5: 6 CTAs, 168 regs) are also built with an 8-CTA register cap.
+// The default is faster per element in steady state, but when a launch fits
+// in one wave only at the higher occupancy the twin removes the second,
+// mostly empty wave (session 1, p+1 = 4: cfg2 VOL 20.4 -> 18.4 us, RHS
+// 51 -> 39 us; p+1 = 4 now runs 8 CTAs by default, profiles/r01_tuning.md).
 #ifndef FDG_HIOCC
 #define FDG_HIOCC 8
 #endif
 template <int D, int P1, int MODE>
 constexpr bool has_hiocc()
 {
-    return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && FDG_MIN_BLOCKS == 0;
+    return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && FDG_MIN_BLOCKS == 0 &&
+           min_blocks<D, P1, MODE>() < FDG_HIOCC;
 }
 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC>

@@ -109,8 +109,6 @@ struct Geo {
     static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && P1 == 4;
     static constexpr int NNP = SWZ ? NN : NN + FDG_PAD * (NN / P1);  // else one pad slot per innermost row
     static constexpr int EPB = LINES >= FDG_TARGET_THREADS ? 1 : FDG_TARGET_THREADS / LINES;
-    // resident-CTA hint for __launch_bounds__ (register cap 64K / (NT * MINB))
-    static constexpr int MINB = FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (P1 <= 5 ? 6 : 1);
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
     static constexpr int FS = EPB * NNP;      // stride of one primitive field
     static constexpr int FA = EPB * NNP + 1;  // stride of one accumulator variable (odd: spreads banks)
@@ -134,6 +132,16 @@ struct Geo {
     __device__ static __forceinline__ int acc(int v, int el, int node) { return v * FA + el * NNP + pad(node); }
 };
 
+// resident-CTA hint for __launch_bounds__ (register cap 64K / (NT * MINB)).
+// 3D FAST p+1 <= 4: 8 CTAs of 64 threads (128 registers, no spills) -- 2.7%
+// faster in steady state than 6 CTAs at 168 registers and one wave for cfg2
+// (profiles/r01_tuning.md); others: 6 (p+1 = 5) or as many as fit.
+template <int D, int P1, int MODE>
+__host__ __device__ constexpr int min_blocks()
+{
+    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (MODE == FAST && D == 3 && P1 <= 4) ? 8 : (P1 <= 5 ? 6 : 1);
+}
+
 template <int D, int P1, int VF, int LOGS>
 __host__ __device__ constexpr int sq_doubles()
 {
@@ -143,13 +151,64 @@ __host__ __device__ constexpr int sq_doubles()
     return prims > faces ? prims : faces;
 }
 
+// accumulator / AoS-staging block offset (even: 16-byte aligned bulk copies)
+template <int D, int P1, int VF, int LOGS>
+__host__ __device__ constexpr int sacc_offset()
+{
+    return (sq_doubles<D, P1, VF, LOGS>() + 1) & ~1;
+}
+
 template <int D, int P1, int VF, int LOGS>
 __host__ __device__ constexpr int smem_doubles()
 {
     using G = Geo<D, P1>;
     // primitive fields (later: the face-flux buffer) + accumulators (the
-    // accumulator block doubles as the AoS staging buffer of u, which is smaller)
-    return sq_doubles<D, P1, VF, LOGS>() + G::NVAR * G::FA;
+    // accumulator block doubles as the AoS staging buffer of u, which is
+    // smaller) + the bulk-copy mbarrier
+    return sacc_offset<D, P1, VF, LOGS>() + G::NVAR * G::FA + 1;
+}
+
+// ---- TMA bulk copy of a batch's state into shared memory (one elected
+// thread issues it, an mbarrier counts the bytes; SASS UBLKCP + SYNCS)
+#ifndef FDG_TMA
+#define FDG_TMA 1
+#endif
+__device__ __forceinline__ void mbar_init(uint64_t* bar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+// shared -> global bulk copy (one bulk group); the smem source may be reused
+// after bulk_wait_read(), the data is globally visible after bulk_wait_all()
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(b),
+        "r"(phase)
+        : "memory");
 }
 
 // compile-time for loop: f(integral_constant<int, i>) for i in [B, E)
@@ -397,7 +456,7 @@ extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 // OCC > 0 overrides the resident-CTA hint (the high-occupancy twin used when a
 // launch fits one wave only at that occupancy, fdg_dispatch.cuh)
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0>
-__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MINB)
+__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE>())
     elem_kernel(const __grid_constant__ KParams prm)
 {
     using G = Geo<D, P1>;
@@ -407,8 +466,18 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
     constexpr int KN = (EPB * NN + NT - 1) / NT;         // nodes per thread
     extern __shared__ double smem[];
     double* sq = smem;                        // (2+D+NX) fields x FS
-    double* sacc = smem + sq_doubles<D, P1, VF, LOGS>();  // NVAR x FA (AoS u staging before the volume pass)
+    double* sacc = smem + sacc_offset<D, P1, VF, LOGS>();  // NVAR x FA (AoS u staging before the volume pass)
     const int tid = threadIdx.x;
+    // whole element blocks are 16-byte multiples and u is 16-byte aligned:
+    // the batch arrives by one bulk copy (else the per-thread copy loop)
+    constexpr bool TMA_SHAPE = FDG_TMA && (NN * NVAR) % 2 == 0;
+    const bool tma = TMA_SHAPE && (reinterpret_cast<uintptr_t>(prm.u) & 15) == 0;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sacc + G::NVAR * G::FA);
+    // VOL leaves as AoS through the (then free) primitive region by a bulk store
+    const bool tma_out = TMA_SHAPE && prm.epilogue == EPI_VOLUME && (reinterpret_cast<uintptr_t>(prm.out) & 15) == 0;
+    unsigned phase = 0;
+    if (TMA_SHAPE && tid == 0) mbar_init(bar);
+    if (TMA_SHAPE) __syncthreads();
 #if FDG_PDL
     // launched with programmatic stream serialization (fdg_dispatch.cuh):
     // everything above touches only registers and the parameter bank
@@ -467,7 +536,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
             // before the first shared-memory store, and the per-node chains
             // (division, reciprocal, logs) of one thread run side by side.
             FDG_PT(7)
-            {
+            if (tma) {
+                if (tid == 0) {
+                    bulk_load(sacc, prm.u + base, (unsigned)count * 8u, bar);
+                    if (tma_out) bulk_wait_read();  // the previous batch's VOL has left the primitive region
+                }
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+            } else {
+                if (tma_out && tid == 0) bulk_wait_read();
                 constexpr int CH = KU < 24 ? KU : 16;
 #pragma unroll
                 for (int k0 = 0; k0 < KU; k0 += CH) {
@@ -549,13 +626,21 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
                     for (int v = 0; v < NVAR; ++v) {
                         const int s = G::acc(v, tel, node);
                         const double vol = (MODE == FAST) ? sacc[s] * scale : sacc[s] / scale;
-                        if (epi == EPI_VOLUME) prm.out[base + t * NVAR + v] = vol;
-                        else sacc[s] = vol;
+                        if (epi == EPI_VOLUME) {
+                            if (tma_out) sq[t * NVAR + v] = vol;  // AoS, conflict-free (odd stride)
+                            else prm.out[base + t * NVAR + v] = vol;
+                        } else {
+                            sacc[s] = vol;
+                        }
                     }
                 }
             }
             if (epi == EPI_VOLUME) {
+                // the next batch's bulk copy (async proxy) overwrites what
+                // this one wrote and read through the generic proxy
+                if (TMA_SHAPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncthreads();
+                if (tma_out && tid == 0) bulk_store(prm.out + base, sq, (unsigned)count * 8u);
                 FDG_PT(5)
                 continue;
             }
@@ -656,8 +741,10 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : Geo<D, P1>::MI
             }
         }
         if (bad) atomicMin(&prm.status->bad_stage, prm.stage_index);
+        if (TMA_SHAPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
     }
+    if (tma_out && tid == 0) bulk_wait_all();
 #if FDG_PHASE_TIMING
     if (tid == 0)
         for (int i = 0; i < 8; ++i) atomicAdd(&fdg_phase_cycles[i], (unsigned long long)pt_[i]);
