@@ -17,11 +17,12 @@ using LaunchFn = cudaError_t (*)(const KParams&, cudaStream_t, int sm_count);
 #ifndef FDG_HIOCC
 #define FDG_HIOCC 8
 #endif
-template <int D, int P1, int MODE>
+template <int D, int P1, int MODE, bool CURVED>
 constexpr bool has_hiocc()
 {
-    return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && FDG_MIN_BLOCKS == 0 &&
-           min_blocks<D, P1, MODE>() < FDG_HIOCC;
+    // (curved kernels spill heavily at 128 registers: no twin)
+    return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && !CURVED && FDG_MIN_BLOCKS == 0 &&
+           min_blocks<D, P1, MODE, CURVED>() < FDG_HIOCC;
 }
 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC>
@@ -70,7 +71,7 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
 {
     using G = Geo<D, P1>;
     constexpr size_t smem = (size_t)smem_doubles<D, P1, VF, LOGS>() * sizeof(double);
-    constexpr bool twin = has_hiocc<D, P1, MODE>();
+    constexpr bool twin = has_hiocc<D, P1, MODE, CURVED>();
     static int bps = -1, bps_hi = -1;  // resident CTAs per SM (one device per process)
     if (bps < 0) {
         cudaError_t err = elem_occupancy<D, P1, VF, CURVED, MODE, LOGS, 0>(&bps);

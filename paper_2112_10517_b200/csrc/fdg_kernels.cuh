@@ -133,13 +133,14 @@ struct Geo {
 };
 
 // resident-CTA hint for __launch_bounds__ (register cap 64K / (NT * MINB)).
-// 3D FAST p+1 <= 4: 8 CTAs of 64 threads (128 registers, no spills) -- 2.7%
-// faster in steady state than 6 CTAs at 168 registers and one wave for cfg2
-// (profiles/r01_tuning.md); others: 6 (p+1 = 5) or as many as fit.
-template <int D, int P1, int MODE>
+// 3D FAST Cartesian p+1 <= 4: 8 CTAs of 64 threads (128 registers, no spills)
+// -- 2.7% faster in steady state than 6 CTAs at 168 registers and one wave for
+// cfg2 (profiles/r01_tuning.md); curved kernels spill at 128 registers;
+// others: 6 (p+1 <= 5) or as many as fit.
+template <int D, int P1, int MODE, bool CURVED>
 __host__ __device__ constexpr int min_blocks()
 {
-    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (MODE == FAST && D == 3 && P1 <= 4) ? 8 : (P1 <= 5 ? 6 : 1);
+    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (MODE == FAST && D == 3 && P1 <= 4 && !CURVED) ? 8 : (P1 <= 5 ? 6 : 1);
 }
 
 template <int D, int P1, int VF, int LOGS>
@@ -376,13 +377,19 @@ __device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, 
 // element); line m of direction n. Same arguments from both adjacent
 // elements, so both see identical bits (discretization.py:730-760 evaluates
 // each face once and scatters both ways).
+template <int D, int P1>
+__device__ __forceinline__ int line_stride(int n)  // P1^(D-1-n) without a runtime power loop
+{
+    return D == 3 ? (n == 0 ? P1 * P1 : (n == 1 ? P1 : 1)) : (n == 0 ? P1 : 1);
+}
+
 template <int D, int P1, bool CURVED, int MODE>
 __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, int n, int side, int m, double* f)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
     constexpr int FN = G::LINES;
-    const int stride = G::stride(n);
+    const int stride = line_stride<D, P1>(n);
     const int hi = m / stride, lo = m - hi * stride;
     const int first = hi * P1 * stride + lo;         // line position 0
     const int last = first + (P1 - 1) * stride;      // line position p
@@ -456,7 +463,7 @@ extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 // OCC > 0 overrides the resident-CTA hint (the high-occupancy twin used when a
 // launch fits one wave only at that occupancy, fdg_dispatch.cuh)
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0>
-__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE>())
+__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE, CURVED>())
     elem_kernel(const __grid_constant__ KParams prm)
 {
     using G = Geo<D, P1>;
@@ -468,13 +475,16 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     double* sq = smem;                        // (2+D+NX) fields x FS
     double* sacc = smem + sacc_offset<D, P1, VF, LOGS>();  // NVAR x FA (AoS u staging before the volume pass)
     const int tid = threadIdx.x;
-    // whole element blocks are 16-byte multiples and u is 16-byte aligned:
-    // the batch arrives by one bulk copy (else the per-thread copy loop)
-    constexpr bool TMA_SHAPE = FDG_TMA && (NN * NVAR) % 2 == 0;
-    const bool tma = TMA_SHAPE && (reinterpret_cast<uintptr_t>(prm.u) & 15) == 0;
+    // full batches are 16-byte multiples (so every batch starts 16-byte
+    // aligned) and u is 16-byte aligned: a batch arrives by one bulk copy
+    // (a ragged last batch of odd size, or a misaligned u: the per-thread
+    // copy loop)
+    constexpr bool TMA_SHAPE = FDG_TMA && (EPB * NN * NVAR) % 2 == 0;
+    const bool tma_u = TMA_SHAPE && (reinterpret_cast<uintptr_t>(prm.u) & 15) == 0;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sacc + G::NVAR * G::FA);
     // VOL leaves as AoS through the (then free) primitive region by a bulk store
-    const bool tma_out = TMA_SHAPE && prm.epilogue == EPI_VOLUME && (reinterpret_cast<uintptr_t>(prm.out) & 15) == 0;
+    const bool tma_out_ok = TMA_SHAPE && prm.epilogue != EPI_STAGE && (reinterpret_cast<uintptr_t>(prm.out) & 15) == 0;
+    bool tma_pending = false;  // a bulk store may still be reading the primitive region
     unsigned phase = 0;
     if (TMA_SHAPE && tid == 0) mbar_init(bar);
     if (TMA_SHAPE) __syncthreads();
@@ -508,6 +518,8 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         const int count = ne * NN * NVAR;
         const long long e = e0 + el;
         const bool active = (el < ne);
+        const bool tma = tma_u && (count % 2) == 0;
+        const bool tma_out = tma_out_ok && (count % 2) == 0;
 
 #if FDG_PREFETCH
         // warm L2 with the next batch of this CTA (its state, and metrics on
@@ -539,12 +551,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             if (tma) {
                 if (tid == 0) {
                     bulk_load(sacc, prm.u + base, (unsigned)count * 8u, bar);
-                    if (tma_out) bulk_wait_read();  // the previous batch's VOL has left the primitive region
+                    if (tma_pending) bulk_wait_read();  // the previous batch's VOL has left the primitive region
                 }
                 mbar_wait(bar, phase);
                 phase ^= 1u;
             } else {
-                if (tma_out && tid == 0) bulk_wait_read();
+                if (tma_pending && tid == 0) bulk_wait_read();
                 constexpr int CH = KU < 24 ? KU : 16;
 #pragma unroll
                 for (int k0 = 0; k0 < KU; k0 += CH) {
@@ -641,11 +653,13 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                 if (TMA_SHAPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncthreads();
                 if (tma_out && tid == 0) bulk_store(prm.out + base, sq, (unsigned)count * 8u);
+                tma_pending = tma_out;
                 FDG_PT(5)
                 continue;
             }
         } else {
             // mesh_surface: accumulate into the caller's array
+            if (tma_pending && tid == 0) bulk_wait_read();  // the outputs are staged in the primitive region
 #pragma unroll
             for (int k = 0; k < KU; ++k) {
                 const int t = tid + k * NT;
@@ -658,67 +672,61 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             }
         }
         __syncthreads();
-        // ---- interface fluxes: every face node of the batch independently
-        // (both sides of an interface evaluate it from identical arguments),
-        // into a face buffer that reuses the primitive-field region
-        {
-            constexpr int KF = (EPB * G::NF + NT - 1) / NT;
-            double* fbuf = sq;
+        // ---- interface terms, direction by direction: every face node of the
+        // batch evaluates its interface flux on its own (both sides of an
+        // interface from identical arguments, no inter-CTA traffic) and lifts
+        // it straight into its node's accumulator. Within one direction a node
+        // lies on at most one face, and the passes keep the reference's
+        // per-node order (n ascending; discretization.py:754-760: out +=
+        // 1/(w_p J) f on the minus side, out -= 1/(w_0 J) f on the plus side).
+        // one copy of the face code (runtime n): three inlined copies spilled
+        // registers in the curved p+1 = 5 kernels
+#pragma unroll 1
+        for (int n = 0; n < D; ++n) {
+            const int stride = line_stride<D, P1>(n);
+            constexpr int NI = 2 * G::LINES;  // face nodes per element in direction n
+            constexpr int KF = (EPB * NI + NT - 1) / NT;
 #pragma unroll(kFaceUnroll)
             for (int k = 0; k < KF; ++k) {
                 const int it = tid + k * NT;
-                if (it < ne * G::NF) {
-                    const int fel = it / G::NF, r = it - fel * G::NF;
-                    const int f = r / G::LINES, mm = r - f * G::LINES;
+                if (it < ne * NI) {
+                    const int fel = it / NI, r = it - fel * NI;
+                    const int side = r / G::LINES, mm = r - side * G::LINES;
                     double fl[NVAR];
-                    face_flux_item<D, P1, CURVED, MODE>(prm, e0 + fel, f >> 1, f & 1, mm, fl);
+                    face_flux_item<D, P1, CURVED, MODE>(prm, e0 + fel, n, side, mm, fl);
+                    const int hi = mm / stride, lo = mm - hi * stride;
+                    const int node = (hi * P1 + (side ? P1 - 1 : 0)) * stride + lo;
+                    const double J = CURVED ? __ldg(prm.jac + (e0 + fel) * NN + node) : prm.jac_const;
+                    if (side) {  // e is the minus element: its +n face
+                        const double sm = 1.0 / (prm.wp * J);
 #pragma unroll
-                    for (int v = 0; v < NVAR; ++v) fbuf[it * NVAR + v] = fl[v];
+                        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, fel, node)] += sm * fl[v];
+                    } else {
+                        const double sp = 1.0 / (prm.w0 * J);
+#pragma unroll
+                        for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, fel, node)] -= sp * fl[v];
+                    }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
-        // ---- per node: VOL + lifted face fluxes in direction order
-        // (discretization.py:754-760: out += 1/(w_p J) f on the minus side,
-        // out -= 1/(w_0 J) f on the plus side), then the outputs
+        // ---- outputs per node
         bool bad = false;
-#pragma unroll 1
+#pragma unroll
         for (int k = 0; k < KN; ++k) {
             const int t = tid + k * NT;
             if (t >= ne * NN) continue;
             const int tel = t / NN, node = t - tel * NN;
-            double val[NVAR];
-#pragma unroll
-            for (int v = 0; v < NVAR; ++v) val[v] = sacc[G::acc(v, tel, node)];
-            const double J = CURVED ? __ldg(prm.jac + e0 * NN + t) : prm.jac_const;
-            const double* fb = sq + tel * G::NF * NVAR;
-#pragma unroll
-            for (int n = 0; n < D; ++n) {
-                const int stride = G::stride(n);
-                const int a = (node / stride) % P1;
-                const int ml = node / (stride * P1) * stride + node % stride;
-                if (a == P1 - 1) {
-                    const double sm = 1.0 / (prm.wp * J);
-                    const double* fv = fb + ((2 * n + 1) * G::LINES + ml) * NVAR;
-#pragma unroll
-                    for (int v = 0; v < NVAR; ++v) val[v] += sm * fv[v];
-                }
-                if (a == 0) {
-                    const double sp = 1.0 / (prm.w0 * J);
-                    const double* fv = fb + ((2 * n) * G::LINES + ml) * NVAR;
-#pragma unroll
-                    for (int v = 0; v < NVAR; ++v) val[v] -= sp * fv[v];
-                }
-            }
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) {
+                const double val = sacc[G::acc(v, tel, node)];
                 const long long g = base + (long long)t * NVAR + v;
-                if (epi == EPI_SURFACE) {
-                    prm.out[g] = val[v];
-                } else if (epi == EPI_RHS) {
-                    prm.out[g] = -val[v];
+                if (epi == EPI_SURFACE || epi == EPI_RHS) {
+                    const double y = (epi == EPI_RHS) ? -val : val;
+                    if (tma_out) sq[t * NVAR + v] = y;  // AoS for the bulk store
+                    else prm.out[g] = y;
                 } else {  // EPI_STAGE
-                    const double kv = -val[v];
+                    const double kv = -val;
                     const double x = __ldg(prm.u + g);
                     double y;
                     if (prm.stage_kind == 0) {
@@ -743,8 +751,10 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         if (bad) atomicMin(&prm.status->bad_stage, prm.stage_index);
         if (TMA_SHAPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
+        if (tma_out && tid == 0) bulk_store(prm.out + base, sq, (unsigned)count * 8u);
+        tma_pending = tma_out;
     }
-    if (tma_out && tid == 0) bulk_wait_all();
+    if (tma_out_ok && tid == 0) bulk_wait_all();
 #if FDG_PHASE_TIMING
     if (tid == 0)
         for (int i = 0; i < 8; ++i) atomicAdd(&fdg_phase_cycles[i], (unsigned long long)pt_[i]);

@@ -10,7 +10,7 @@ HERE=$(pwd)
 UNIT=$1; shift
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 COMMON="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC"
-rm -rf obj_var; mkdir -p ../variants obj_var
+mkdir -p ../variants obj_var
 {
   echo '#include "../fdg_dispatch.cuh"'
   for m in faithful fast; do for d in 2 3; do for p in 2 3 4 5 6 7 8; do

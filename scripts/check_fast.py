@@ -8,7 +8,8 @@ import numpy as np  # noqa: E402
 from oracle import oracle  # noqa: E402
 from paper_2112_10517_b200 import RhsConfig, mesh_fluxdiff_volume, rhs, workloads  # noqa: E402
 
-for cfg, dims in ((2, (4, 4, 4)), (2, (6, 5, 4))):
+CFG = int(os.environ.get("CHECK_CFG", "2"))  # BASELINE config whose degree the variant lib holds
+for cfg, dims in ((CFG, (4, 4, 4)), (CFG, (6, 5, 4))):
     setup, u, _ = workloads.build(cfg, dims=dims)
     for pre in ("primitives_and_logs", "none"):
         c = RhsConfig(volume_flux="ranocha", surface_flux="llf", precompute=pre, kernel="batched")
