@@ -328,6 +328,103 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
         for (int v = 0; v < NVAR; ++v) sacc[G::acc(v, el, nodes[a])] = acc[a][v];
 }
 
+template <int D, int P1>
+__device__ __forceinline__ int line_stride(int n)  // P1^(D-1-n) without a runtime power loop
+{
+    return D == 3 ? (n == 0 ? P1 * P1 : (n == 1 ? P1 : 1)) : (n == 0 ? P1 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// FAST volume pass with a RUNTIME direction n: one copy of the pair code for
+// all d directions (the compile-time passes triple the kernel's SASS: 190 KB
+// at p+1 = 8, where ncu showed 10.8% "no instruction" stalls). Cartesian
+// meshes load every node's velocity ROTATED, v'_j = v_{(n+j) mod d}, and call
+// the axis-0 flux: for an axis-aligned direction the fluxes are rotation
+// covariant, so the rotated momentum components come out in the same slots
+// and go back to their variables through the same map when the accumulators
+// are loaded and stored (addresses only, no selects). Curved meshes use the
+// general-normal flux with the direction's metric row. Not for FAITHFUL (the
+// rotation reorders dot-product sums) nor the central flux (its staged
+// conserved momenta would need the same rotation).
+#ifndef FDG_RT_DIR_MIN_P1
+#define FDG_RT_DIR_MIN_P1 5  // p+1 = 4: 7% slower; 5: cfg4 RHS +5%; 8: cfg3 +3-16% (profiles/r01_tuning.md)
+#endif
+template <int D, int P1, int VF>
+__host__ __device__ constexpr bool runtime_direction()
+{
+    return P1 >= FDG_RT_DIR_MIN_P1 && VF != F_CENTRAL;
+}
+
+template <int D, int P1, int VF, bool CURVED, int LOGS>
+__device__ __forceinline__ void volume_direction_rt(const KParams& prm, const double* sq, double* sacc, int el, int m,
+                                                    long long e, int n, unsigned vm)
+{
+    using G = Geo<D, P1>;
+    constexpr int NVAR = G::NVAR;
+    constexpr int NX = n_extra(VF, LOGS);
+    const int stride = line_stride<D, P1>(n);
+    const int base = (m / stride) * P1 * stride + m % stride;  // line position 0
+    // variable / field index of rotated slot j (rho, v'_0..v'_{d-1}, E | p, extras)
+    int vmap[NVAR];
+    vmap[0] = 0;
+    vmap[NVAR - 1] = NVAR - 1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) vmap[1 + j] = CURVED ? 1 + j : 1 + (n + j) % D;
+    double acc[P1][NVAR];
+#pragma unroll
+    for (int a = 0; a < P1; ++a) {
+        const int nd = base + a * stride;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) acc[a][v] = (n == 0) ? 0.0 : sacc[G::acc(vmap[v], el, nd)];
+    }
+    const int sbase = el * G::NNP;
+    auto load = [&](int a) {
+        const int idx = sbase + G::pad(base + a * stride);
+        Node<D, NX> q;
+        q.rho = sq[idx];
+#pragma unroll
+        for (int j = 0; j < D; ++j) q.v[j] = sq[vmap[1 + j] * G::FS + idx];
+        q.p = sq[(1 + D) * G::FS + idx];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) q.x[k] = sq[(2 + D + k) * G::FS + idx];
+        if constexpr (NX == 0) q.x[0] = 0.0;
+        return q;
+    };
+    const double* w = prm.wts[n];
+    sfor<0, P1>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        const Node<D, NX> qa = load(a);
+        sfor<a + 1, P1>([&](auto B) {
+            constexpr int b = decltype(B)::value;
+            const Node<D, NX> qb = load(b);
+            const double wa = w[a * P1 + b];
+            const double wb = w[b * P1 + a];
+            double f[NVAR];
+            if constexpr (CURVED) {
+                double alpha[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    alpha[j] = 0.5 * (__ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j) +
+                                      __ldg(prm.ja + ((e * G::NN + base + b * stride) * D + n) * D + j));
+                fast_volume_flux<D, VF, -1, LOGS>(qa, qb, alpha, prm.gas.igm1, f, vm);
+            } else {
+                fast_volume_flux<D, VF, 0, LOGS>(qa, qb, nullptr, prm.gas.igm1, f, vm);
+            }
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                acc[a][v] = fma(wa, f[v], acc[a][v]);
+                acc[b][v] = fma(wb, f[v], acc[b][v]);
+            }
+        });
+    });
+#pragma unroll
+    for (int a = 0; a < P1; ++a) {
+        const int nd = base + a * stride;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) sacc[G::acc(vmap[v], el, nd)] = acc[a][v];
+    }
+}
+
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
 __device__ __forceinline__ void vdir(const KParams& prm, const double* sq, double* sacc, int el, int m, long long e,
                                      bool active, unsigned vm)
@@ -377,11 +474,6 @@ __device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, 
 // element); line m of direction n. Same arguments from both adjacent
 // elements, so both see identical bits (discretization.py:730-760 evaluates
 // each face once and scatters both ways).
-template <int D, int P1>
-__device__ __forceinline__ int line_stride(int n)  // P1^(D-1-n) without a runtime power loop
-{
-    return D == 3 ? (n == 0 ? P1 * P1 : (n == 1 ? P1 : 1)) : (n == 0 ? P1 : 1);
-}
 
 template <int D, int P1, bool CURVED, int MODE>
 __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, int n, int side, int m, double* f)
@@ -610,15 +702,23 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             __syncthreads();
             FDG_PT(1)
             // ---- volume integral, direction by direction (accumulators: SoA)
-            vdir<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e, active, vmask);
-            __syncthreads();
-            FDG_PT(2)
-            vdir<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e, active, vmask);
-            __syncthreads();
-            FDG_PT(3)
-            if constexpr (D == 3) {
-                vdir<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e, active, vmask);
+            if constexpr (MODE == FAST && runtime_direction<D, P1, VF>()) {
+#pragma unroll 1
+                for (int n = 0; n < D; ++n) {
+                    if (vmask) volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, vmask);
+                    __syncthreads();
+                }
+            } else {
+                vdir<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e, active, vmask);
                 __syncthreads();
+                FDG_PT(2)
+                vdir<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e, active, vmask);
+                __syncthreads();
+                FDG_PT(3)
+                if constexpr (D == 3) {
+                    vdir<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e, active, vmask);
+                    __syncthreads();
+                }
             }
             FDG_PT(4)
             // ---- VOL = acc / J   (FAITHFUL: the reference's division, out /= jac;
