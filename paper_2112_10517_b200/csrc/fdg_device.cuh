@@ -78,6 +78,16 @@ __device__ __forceinline__ double rcp_fast(double x)
     return fma(r, fma(e, e, e), r);
 }
 
+// ~1 ulp 1/sqrt(x), x > 0 normal, branch free (FAST mode only): MUFU.RSQ64H
+// and one cubically convergent correction r (1 + e/2 + 3e^2/8), e = 1 - x r^2
+__device__ __forceinline__ double rsqrt_fast(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x * r, r, 1.0);
+    return fma(r, e * fma(0.375, e, 0.5), r);
+}
+
 template <int MODE>
 __device__ __forceinline__ double dlog(double x)
 {
@@ -546,7 +556,7 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
     }
     const double p_l = gas.gm1 * fma(-0.5, kl, ul[D + 1]);
     const double p_r = gas.gm1 * fma(-0.5, kr, ur[D + 1]);
-    double norm, vns_l, vns_r;  // |n| and v.n with the scaled normal
+    double norm, vns_l, vns_r, inorm_ = 0.0;  // |n| and v.n with the scaled normal
     if constexpr (AXIS >= 0) {
         norm = nrm[AXIS];
         vns_l = vl[AXIS] * norm;
@@ -561,11 +571,15 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
             vns_l = fma(vl[i], nrm[i], vns_l);
             vns_r = fma(vr[i], nrm[i], vns_r);
         }
-        norm = sqrt(nn);
+        inorm_ = rsqrt_fast(nn);
+        norm = nn * inorm_;
     }
-    const double inorm = rcp_fast(norm);
-    const double lam_l = fma(fabs(vns_l), inorm, sqrt(gas.gamma * p_l * ril));
-    const double lam_r = fma(fabs(vns_r), inorm, sqrt(gas.gamma * p_r * rir));
+    const double inorm = (AXIS >= 0) ? rcp_fast(norm) : inorm_;
+    // sound speeds sqrt(gamma p / rho) as x rsqrt(x): no IEEE sqrt slow path
+    // (admissible states have p, rho > 0; the gate reports the others)
+    const double cl2 = gas.gamma * p_l * ril, cr2 = gas.gamma * p_r * rir;
+    const double lam_l = fma(fabs(vns_l), inorm, cl2 * rsqrt_fast(cl2));
+    const double lam_r = fma(fabs(vns_r), inorm, cr2 * rsqrt_fast(cr2));
     const double halfdiss = 0.5 * fmax(lam_l, lam_r) * norm;
     f[0] = 0.5 * (ul[0] * vns_l + ur[0] * vns_r) - halfdiss * (ur[0] - ul[0]);
 #pragma unroll

@@ -106,7 +106,9 @@ struct Geo {
 #ifndef FDG_SWIZZLE
 #define FDG_SWIZZLE 1
 #endif
-    static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && P1 == 4;
+    // (p + 1 = 8: bank pair (node & 15) ^ ((node >> 3) & 15), the same property
+    // for the 32 lines of a warp; profiles/r01_tuning.md)
+    static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && (P1 == 4 || P1 == 8);
     static constexpr int NNP = SWZ ? NN : NN + FDG_PAD * (NN / P1);  // else one pad slot per innermost row
     static constexpr int EPB = LINES >= FDG_TARGET_THREADS ? 1 : FDG_TARGET_THREADS / LINES;
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
@@ -125,7 +127,8 @@ struct Geo {
     }
     __device__ static __forceinline__ int pad(int node)
     {
-        if constexpr (SWZ) return node ^ (((node >> 4) * 5) & 15);  // bank pair (node & 15) ^ 5 (node >> 4)
+        if constexpr (SWZ && P1 == 4) return node ^ (((node >> 4) * 5) & 15);  // bank pair (node & 15) ^ 5 (node >> 4)
+        else if constexpr (SWZ) return node ^ ((node >> 3) & 15);
         else return FDG_PAD ? node + node / P1 : node;
     }
     // accumulator slot of (variable v, element el, node)
