@@ -65,10 +65,10 @@ struct KParams {
     double sa, sb, sc, dt;    // 2N: a_i, b_i, -, dt ; SO: A, B, C*dt, -
 };
 
-// tuning knobs (compile-time; scripts/variants.sh builds alternatives)
-// Defaults measured on B200 (scripts/variants.sh + scripts/sweep.py):
-// 64-thread CTAs and a register cap that keeps 6 CTAs resident for p <= 4
-// (cfg2 16^3: 10.7 -> 12.8 G nodes/s, 64^3: 21.9 -> 22.5).
+// tuning knobs (compile-time; scripts/ab.sh builds alternatives). Defaults
+// measured on B200 (scripts/ab.sh + scripts/sweep.py, profiles/r01_tuning.md):
+// 64-thread CTAs (one warp for 3D p+1 = 4, Geo::TT) and the register caps of
+// min_blocks().
 #ifndef FDG_TARGET_THREADS
 #define FDG_TARGET_THREADS 64
 #endif
@@ -110,7 +110,11 @@ struct Geo {
     // for the 32 lines of a warp; profiles/r01_tuning.md)
     static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && (P1 == 4 || P1 == 8);
     static constexpr int NNP = SWZ ? NN : NN + FDG_PAD * (NN / P1);  // else one pad slot per innermost row
-    static constexpr int EPB = LINES >= FDG_TARGET_THREADS ? 1 : FDG_TARGET_THREADS / LINES;
+    // threads per CTA target: one warp (2 elements) for 3D p+1 = 4 -- no
+    // barrier coupling between warps, cfg2 VOL +1.3%, RHS +3.7% against 2-warp
+    // CTAs (profiles/r01_tuning.md) -- else FDG_TARGET_THREADS
+    static constexpr int TT = (D == 3 && P1 == 4 && FDG_TARGET_THREADS == 64) ? 32 : FDG_TARGET_THREADS;
+    static constexpr int EPB = LINES >= TT ? 1 : TT / LINES;
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
     static constexpr int FS = EPB * NNP;      // stride of one primitive field
     static constexpr int FA = EPB * NNP + 1;  // stride of one accumulator variable (odd: spreads banks)
@@ -143,7 +147,10 @@ struct Geo {
 template <int D, int P1, int MODE, bool CURVED>
 __host__ __device__ constexpr int min_blocks()
 {
-    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (MODE == FAST && D == 3 && P1 <= 4 && !CURVED) ? 8 : (P1 <= 5 ? 6 : 1);
+    // counted in 64-thread CTAs, scaled to the CTA size (same warps per SM)
+    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS
+                              : ((MODE == FAST && D == 3 && P1 <= 4 && !CURVED) ? 8 : (P1 <= 5 ? 6 : 1)) *
+                                    (Geo<D, P1>::NT < 64 ? 64 / Geo<D, P1>::NT : 1);
 }
 
 template <int D, int P1, int VF, int LOGS>
