@@ -203,6 +203,24 @@ def run_reference(args, rank, world):
     return 0
 
 
+def _gpu_local_cpus(index):
+    """Host CPUs NVML reports as local to GPU `index` (its NUMA node), or None."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            n = os.cpu_count() or 64
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        finally:
+            pynvml.nvmlShutdown()
+        cpus = {64 * w + b for w, mask in enumerate(words) for b in range(64) if (int(mask) >> b) & 1}
+        return cpus or None
+    except Exception:
+        return None
+
+
 def _traffic_from_profile():
     """dram bytes per launch of the volume kernel from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "vol_cfg2_ncu_summary.json")
@@ -407,23 +425,36 @@ def main():
     del flush, graph
 
     # ---- end to end through the public API with pinned host buffers
-    # pinned input filled by pin_memory()'s own copy: a multithreaded torch
-    # copy_ into an existing pinned buffer left its H2D at ~0.38-0.46 ms
-    # instead of 0.20 ms on the same box (scripts/e2e_probe.py,
-    # profiles/r01_e2e.md); the fill is setup, outside the timed region
-    u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
-    out_pin = torch.empty(u_host.shape, dtype=torch.float64, pin_memory=True)
-    for _ in range(max(args.warmup, 3)):
-        mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
-    e2e_ms = []
-    for _ in range(args.steps):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
-        b.record(stream)
-        b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
+    # The pinned buffers are allocated (pages placed) and the e2e loop runs on
+    # the GPU's NUMA-local CPUs (NVML CPU affinity): a remote-socket buffer
+    # halves the H2D rate on some hosts. The affinity is restored afterwards
+    # (the CPU baseline below uses every host thread).
+    cpus_all = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    cpus_near = _gpu_local_cpus(local)
+    if cpus_near and cpus_all:
+        cpus_near &= cpus_all
+        if cpus_near:
+            os.sched_setaffinity(0, cpus_near)
+    try:
+        # page-locked by cudaHostAlloc (libfdg fdg_host_alloc): caching-allocator
+        # pinned blocks ran H2D at 0.20-0.74 ms for the same 10.5 MB on one box
+        u_pin = N.pinned_empty(u_host.shape)
+        np.copyto(u_pin.numpy(), u_host)
+        out_pin = N.pinned_empty(u_host.shape)
+        for _ in range(max(args.warmup, 3)):
+            mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
+        e2e_ms = []
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            mesh_fluxdiff_volume(u_pin, setup, config, out=out_pin)
+            b.record(stream)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+    finally:
+        if cpus_near and cpus_all:
+            os.sched_setaffinity(0, cpus_all)
     e2e = statistics.mean(e2e_ms)
     if dist is not None:
         t = torch.tensor([e2e], device="cuda", dtype=torch.float64)
@@ -479,6 +510,8 @@ def main():
             "ms_per_step": e2e,
             "h2d_bytes_per_step": int(u_host.nbytes),
             "d2h_bytes_per_step": int(u_host.nbytes),
+            "host_cpus": "GPU-local (NVML affinity, %d CPUs) for the pinned buffers and the loop" % len(cpus_near)
+            if cpus_near else "process default",
             "ms_min": min(e2e_ms),
             "ms_median": statistics.median(e2e_ms),
             "path": "paper_2112_10517_b200.mesh_fluxdiff_volume(pinned CPU tensor, out=pinned) -> libfdg.so "

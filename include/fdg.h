@@ -101,6 +101,11 @@ int fdg_abi_version(void);
 const char *fdg_last_error(void);
 int fdg_supported(int32_t d, int32_t degree);
 unsigned long long fdg_launch_count(void);
+/* page-locked host buffers for fdg_volume_host (cudaHostAlloc): the copy
+ * engines reach ~54 GB/s H2D on them on every B200 host measured, against
+ * 14-54 GB/s for caching-allocator pinned blocks (profiles/r01_e2e.md) */
+int fdg_host_alloc(size_t bytes, void **out);
+int fdg_host_free(void *ptr);
 
 int fdg_mesh_create(const fdg_mesh_desc_t *desc, fdg_mesh_t **out);
 void fdg_mesh_destroy(fdg_mesh_t *mesh);

@@ -77,6 +77,8 @@ EXPORTS = (
     "fdg_last_error",
     "fdg_supported",
     "fdg_launch_count",
+    "fdg_host_alloc",
+    "fdg_host_free",
     "fdg_mesh_create",
     "fdg_mesh_destroy",
     "fdg_volume",
@@ -113,6 +115,8 @@ def lib():
     L.fdg_last_error.restype = ctypes.c_char_p
     L.fdg_supported.argtypes = [i32, i32]
     L.fdg_launch_count.restype = ctypes.c_ulonglong
+    L.fdg_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    L.fdg_host_free.argtypes = [ctypes.c_void_p]
     L.fdg_mesh_create.argtypes = [P(MeshDesc), P(vp)]
     L.fdg_mesh_destroy.argtypes = [vp]
     L.fdg_mesh_destroy.restype = None
@@ -146,6 +150,26 @@ def check(rc):
 
 def launch_count():
     return int(lib().fdg_launch_count())
+
+
+def pinned_empty(shape, dtype="float64"):
+    """torch CPU tensor on a cudaHostAlloc buffer (fdg_host_alloc), freed with
+    the tensor: the host-buffer path's copies run at the copy engines' full
+    rate on it (profiles/r01_e2e.md)."""
+    import weakref
+
+    import numpy as np
+    import torch
+
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape))
+    ptr = ctypes.c_void_p()
+    check(lib().fdg_host_alloc(n * dt.itemsize, ctypes.byref(ptr)))
+    buf = (ctypes.c_char * max(n * dt.itemsize, 1)).from_address(ptr.value)
+    arr = np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
+    t = torch.from_numpy(arr)
+    weakref.finalize(arr, lib().fdg_host_free, ptr)
+    return t
 
 
 def fp64_peak_tflops(stream=None):

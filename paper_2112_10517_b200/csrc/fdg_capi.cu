@@ -62,6 +62,23 @@ int fdg_supported(int32_t d, int32_t degree) { return (d == 2 || d == 3) && degr
 
 unsigned long long fdg_launch_count(void) { return g_launches.load(); }
 
+int fdg_host_alloc(size_t bytes, void** out)
+{
+    if (!out) return fail(FDG_ERR_ARG, "fdg_host_alloc: null argument");
+    *out = nullptr;
+    cudaError_t err = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaHostAlloc");
+    return FDG_OK;
+}
+
+int fdg_host_free(void* ptr)
+{
+    if (!ptr) return FDG_OK;
+    cudaError_t err = cudaFreeHost(ptr);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaFreeHost");
+    return FDG_OK;
+}
+
 int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
 {
     if (!desc || !out) return fail(FDG_ERR_ARG, "fdg_mesh_create: null argument");

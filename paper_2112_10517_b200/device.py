@@ -148,7 +148,7 @@ class DeviceMesh:
         """Pinned host buffer reused across calls (no allocation on the hot path)."""
         buf = self._staging.get(key)
         if buf is None or tuple(buf.shape) != tuple(shape):
-            buf = self.torch.empty(shape, dtype=self.torch.float64, pin_memory=True)
+            buf = N.pinned_empty(shape)  # cudaHostAlloc: full-rate copies (profiles/r01_e2e.md)
             self._staging[key] = buf
         return buf
 

@@ -62,6 +62,13 @@ def main():
             lambda: (dm.reset_status(), dm.volume_host(u_pin, cfg.scheme(), o_pin, n_chunks=nc))
         )
     res["api_e2e_ms"] = timed(lambda: P.mesh_fluxdiff_volume(u_pin, setup, cfg, out=o_pin))
+    # library-allocated page-locked buffers (fdg_host_alloc / cudaHostAlloc)
+    ul = P._native.pinned_empty(u.shape)
+    ul.numpy()[...] = u
+    ol = P._native.pinned_empty(u.shape)
+    res["libpinned_h2d_ms"] = timed(lambda: ud.copy_(ul, non_blocking=True))
+    res["libpinned_d2h_ms"] = timed(lambda: ol.copy_(vd, non_blocking=True))
+    res["libpinned_api_e2e_ms"] = timed(lambda: P.mesh_fluxdiff_volume(ul, setup, cfg, out=ol))
     # bench.py's buffers: torch.empty(pin_memory=True) + copy_
     u2 = torch.empty(u.shape, dtype=torch.float64, pin_memory=True)
     u2.copy_(torch.from_numpy(u))
