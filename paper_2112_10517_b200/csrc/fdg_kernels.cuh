@@ -109,7 +109,11 @@ struct Geo {
     // (p + 1 = 8: bank pair (node & 15) ^ ((node >> 3) & 15), the same property
     // for the 32 lines of a warp; profiles/r01_tuning.md)
     static constexpr bool SWZ = FDG_SWIZZLE && D == 3 && (P1 == 4 || P1 == 8);
-    static constexpr int NNP = SWZ ? NN : NN + FDG_PAD * (NN / P1);  // else one pad slot per innermost row
+    // other 3D degrees: plain node order -- the pad slot per innermost row
+    // costs more conflicts than it removes there (scripts/bank_model.py:
+    // p+1 = 3/5/7: 5.7/3.7/6.5 -> 3.3/2.7/3.0 wavefronts per warp load)
+    static constexpr bool PADDED = FDG_PAD && !SWZ && !(FDG_SWIZZLE && D == 3);
+    static constexpr int NNP = PADDED ? NN + NN / P1 : NN;  // one pad slot per innermost row
     // threads per CTA target: one warp (2 elements) for 3D p+1 = 4 -- no
     // barrier coupling between warps, cfg2 VOL +1.3%, RHS +3.7% against 2-warp
     // CTAs (profiles/r01_tuning.md) -- else FDG_TARGET_THREADS
@@ -133,7 +137,7 @@ struct Geo {
     {
         if constexpr (SWZ && P1 == 4) return node ^ (((node >> 4) * 5) & 15);  // bank pair (node & 15) ^ 5 (node >> 4)
         else if constexpr (SWZ) return node ^ ((node >> 3) & 15);
-        else return FDG_PAD ? node + node / P1 : node;
+        else return PADDED ? node + node / P1 : node;
     }
     // accumulator slot of (variable v, element el, node)
     __device__ static __forceinline__ int acc(int v, int el, int node) { return v * FA + el * NNP + pad(node); }
