@@ -19,7 +19,8 @@ struct fdg_mesh {
     bool curved = false;
     int sm_count = 148;
     KParams base{};
-    Status* status = nullptr;  // device
+    Status* status = nullptr;       // device
+    Status* status_host = nullptr;  // page-locked read-back slot (a pageable D2H target is a slow, bounced copy)
     // host-buffer pipeline (fdg_volume_host): two copy streams + events, made on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_start = nullptr, ev_done = nullptr;
@@ -149,6 +150,7 @@ void fdg_mesh_destroy(fdg_mesh_t* m)
 {
     if (!m) return;
     if (m->status) cudaFree(m->status);
+    if (m->status_host) cudaFreeHost(m->status_host);
     if (m->s_in) cudaStreamDestroy(m->s_in);
     if (m->s_out) cudaStreamDestroy(m->s_out);
     for (cudaEvent_t e : {m->ev_start, m->ev_done})
@@ -294,17 +296,32 @@ int fdg_volume_host(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u_host, 
     rc = pipeline_init(m);
     if (rc) return rc;
     const long long elem_bytes = nodes_per_elem(m) * (m->d + 2) * (long long)sizeof(double);
-    // default: >= 4 MB chunks, 2..16 of them.  Every chunk costs ~20 us of copy
-    // setup on B200/PCIe5 (profiles/r01_e2e.md: 2 chunks beat 10 on a 10 MB state)
-    if (n_chunks <= 0) n_chunks = (int32_t)std::max<long long>(2, std::min<long long>(16, m->n_elem * elem_bytes >> 22));
+    // default: 4 tapered chunks up to 64 MB, then one per 16 MB (<= 16); every
+    // chunk costs ~10-20 us of copy setup on B200/PCIe5 (profiles/r01_e2e.md:
+    // cfg2's 10.5 MB state, 2 equal chunks 0.361 ms, 4 tapered 0.353, 8: 0.399)
+    if (n_chunks <= 0) {
+        const long long bytes = m->n_elem * elem_bytes;
+        n_chunks = bytes < (4LL << 20) ? 2 : (int32_t)std::max<long long>(4, std::min<long long>(16, bytes >> 24));
+    }
     n_chunks = (int32_t)std::min<long long>(std::min<long long>(n_chunks, kMaxChunks), m->n_elem);
     cudaStream_t st = (cudaStream_t)stream;
     // both copy streams start after everything already queued on `stream`
     cudaError_t err = cudaEventRecord(m->ev_start, st);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(m->s_in, m->ev_start, 0);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(m->s_out, m->ev_start, 0);
+    // tapered chunks: the first chunk's H2D and the last chunk's D2H are the
+    // only copies nothing overlaps, so with 3+ chunks those two are half the
+    // size of the others (weights 1/2, 1, ..., 1, 1/2)
+    const long long W2 = n_chunks >= 3 ? 2LL * (n_chunks - 1) : 2LL * n_chunks;  // total weight x 2
+    auto edge = [&](int c) -> long long {  // element index where chunk c starts
+        if (c <= 0) return 0;
+        if (c >= n_chunks) return m->n_elem;
+        const long long w = n_chunks >= 3 ? 2LL * c - 1 : 2LL * c;
+        return m->n_elem * w / W2;
+    };
     for (int c = 0; c < n_chunks && err == cudaSuccess; ++c) {
-        const long long lo = m->n_elem * c / n_chunks, hi = m->n_elem * (c + 1) / n_chunks;
+        const long long lo = edge(c), hi = edge(c + 1);
+        if (lo == hi) continue;
         const size_t off = (size_t)(lo * elem_bytes / (long long)sizeof(double));
         const size_t bytes = (size_t)((hi - lo) * elem_bytes);
         err = cudaMemcpyAsync(u_dev + off, u_host + off, bytes, cudaMemcpyHostToDevice, m->s_in);
@@ -419,10 +436,13 @@ int fdg_reset_status(fdg_mesh_t* m, void* stream)
 int fdg_read_status(fdg_mesh_t* m, fdg_status_t* out, void* stream)
 {
     if (!m || !out) return fail(FDG_ERR_ARG, "fdg_read_status: null argument");
-    Status h;
-    cudaError_t err = cudaMemcpyAsync(&h, m->status, sizeof(Status), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    cudaError_t err = cudaSuccess;
+    if (!m->status_host) err = cudaHostAlloc(&m->status_host, sizeof(Status), cudaHostAllocDefault);
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(m->status_host, m->status, sizeof(Status), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize((cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "status read");
+    const Status h = *m->status_host;
     out->first_bad = (h.first_bad == ~0ULL) ? -1 : (int64_t)h.first_bad;
     out->bad_stage = (h.bad_stage == ~0U) ? -1 : (int32_t)h.bad_stage;
     out->pad = 0;

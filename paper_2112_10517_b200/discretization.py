@@ -220,11 +220,17 @@ def _count(counter, two_point, logmean):
     _fluxes.bump(counter, two_point=two_point, logmean=logmean)
 
 
+_PAIR_COUNTS = {}  # id(dsplit matrix) -> (matrix, pair count): the counters need it every call
+
+
 def _volume_counts(setup, vol_flux):
     d = setup.d
     p1 = setup.op.degree + 1
-    n_pairs = len(pair_table(np.asarray(setup.dsplit.matrix)))
-    two_point = setup_n_elements(setup) * d * p1 ** (d - 1) * n_pairs
+    mat = setup.dsplit.matrix
+    hit = _PAIR_COUNTS.get(id(mat))
+    if hit is None or hit[0] is not mat:
+        hit = _PAIR_COUNTS[id(mat)] = (mat, len(pair_table(np.asarray(mat))))
+    two_point = setup_n_elements(setup) * d * p1 ** (d - 1) * hit[1]
     logmean = 2 * two_point if vol_flux in ("ranocha", "chandrashekar") else 0
     return two_point, logmean
 
