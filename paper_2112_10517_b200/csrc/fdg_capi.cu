@@ -142,6 +142,12 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         return cuda_fail(err, "cudaMemset(status)");
     }
     k.status = m->status;
+    {
+        long long nn = 1;
+        for (int i = 0; i < m->d; ++i) nn *= m->p1;
+        const double state_bytes = (double)m->n_elem * (double)nn * (m->d + 2) * 8.0;
+        k.face_prefetch = state_bytes > 8.0 * 126.0 * 1024 * 1024;  // >> the 126 MB L2
+    }
     *out = m;
     return FDG_OK;
 }

@@ -61,6 +61,7 @@ struct KParams {
     int surface_flux;
     int precompute;
     int stage_kind;           // 0: low-storage 2N, 1: Shu-Osher convex combination
+    int face_prefetch;        // interface epilogues: prefetch neighbour face rows (state >> L2)
     unsigned int stage_index;
     double sa, sb, sc, dt;    // 2N: a_i, b_i, -, dt ; SO: A, B, C*dt, -
 };
@@ -91,6 +92,9 @@ constexpr int kFaceUnroll = FDG_FACE_UNROLL;
 #endif
 #ifndef FDG_PREFETCH
 #define FDG_PREFETCH 1
+#endif
+#ifndef FDG_FACE_PREFETCH
+#define FDG_FACE_PREFETCH 1  // neighbour face rows into L2 at batch start (interface epilogues)
 #endif
 #ifndef FDG_PDL
 #define FDG_PDL 0  // 1: programmatic dependent launch (fdg_dispatch.cuh); measured no gain in a CUDA graph
@@ -644,6 +648,40 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                     const int b1 = (int)(ne2 * NN * D * D * 8);
                     for (int off = tid * 128; off < b1; off += NT * 128)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(p1 + off));
+                }
+            }
+        }
+#endif
+#if FDG_FACE_PREFETCH
+        // interface epilogues on states much larger than L2 (prm.face_prefetch,
+        // set at mesh creation): warm L2 with the face rows of this batch's
+        // neighbours in directions 0 and 1 now, so the face phase (after the
+        // volume passes) finds them there. Those neighbours are far ahead /
+        // behind in the traversal (128^3: +-16384 and +-128 elements) and
+        // their face loads went to DRAM (cfg5 RHS: 12.6 GB read per launch for
+        // a 5.4 GB state; the prefetch: 10.45 -> 9.93 ms; on L2-resident
+        // meshes it costs 1-3%). Direction-2 neighbours are adjacent elements.
+        if (prm.face_prefetch && epi != EPI_VOLUME && D == 3) {
+            constexpr int NFP = EPB * 4;  // (element, neighbour) items: -0, +0, -1, +1
+            for (int it = tid; it < NFP; it += NT) {
+                const int fel = it >> 2, which = it & 3, n = which >> 1, plus = which & 1;
+                if (fel < ne) {
+                    const int nb = __ldg((plus ? prm.plus : prm.minus) + n * prm.n_elem + e0 + fel);
+                    if (nb >= 0) {
+                        // the neighbour's face adjacent to e: position 0 (plus
+                        // neighbour) or P1-1 (minus neighbour) along direction n
+                        constexpr int S0 = P1 * P1;
+                        const int stride = n == 0 ? S0 : P1;
+                        const int a = plus ? 0 : P1 - 1;
+                        const char* blk = reinterpret_cast<const char*>(prm.u + (long long)nb * NN * NVAR);
+                        const int runs = n == 0 ? 1 : P1, run_nodes = n == 0 ? S0 : P1;
+                        for (int r = 0; r < runs; ++r) {
+                            const int node0 = (r * P1 + a) * stride;  // (hi, a, lo = 0)
+                            const char* p = blk + (long long)node0 * NVAR * 8;
+                            for (int off = 0; off < run_nodes * NVAR * 8; off += 128)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+                        }
+                    }
                 }
             }
         }

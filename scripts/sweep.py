@@ -75,6 +75,7 @@ def main():
         (4, None, "kennedy_gruber", "batched", "none", "rhs"),
         (4, None, "ranocha", "batched", "primitives_and_logs", "volume"),
         (1, None, "ranocha", "batched", "primitives_and_logs", "rhs"),
+        (5, None, "ranocha", "batched", "primitives_and_logs", "rhs"),
     ]
     if args.cases != "all":
         keep = set(int(x) for x in args.cases.split(","))
