@@ -541,7 +541,7 @@ __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, 
 }
 
 #if FDG_PHASE_TIMING
-// profiling build only (scripts/variants.sh): SM cycles per phase, summed over CTAs/batches
+// profiling build only (scripts/ab.sh "pt:.:-DFDG_PHASE_TIMING=1"): SM cycles per phase, summed over CTAs/batches
 __device__ unsigned long long fdg_phase_cycles[8];
 __device__ unsigned long long fdg_cta_ns[3 * 8192];  // per-CTA globaltimer start/end, SM id
 extern "C" int fdg_debug_phase_cycles(unsigned long long* out, int reset)
