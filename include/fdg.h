@@ -15,10 +15,15 @@
  *                    (and of SSPRK43, which the reference does not ship)
  *   fdg_gate      <- discretization._admissibility_gate                  discretization.py:660-672
  *   fdg_mesh_create <- the device image of build_setup's SpatialSetup    discretization.py:609-657
+ *   fdg_diagnostic  <- discretization.conserved_totals                   discretization.py:1027-1031
+ *                      discretization.entropy_rate (its two sums)        discretization.py:1011-1024
+ *                      discretization.error_norm_l2 (before the sqrt)     discretization.py:1033-1037
+ *                      timeint.stable_dt (before the cfl factor)         timeint.py:138-146
  *
  * Conventions: all state pointers are DEVICE pointers owned by the caller
  * (torch allocations in the Python host layer); the library allocates only a
- * 16-byte status record per mesh handle, at creation.  Calls are
+ * 16-byte status record per mesh handle, at creation (and, on the first
+ * fdg_diagnostic call, a few KB of per-block partials).  Calls are
  * stream-ordered and asynchronous; only fdg_read_status synchronizes.
  * Layout: the reference's own AoS layout, u[e][i][v] = (n_elem, (p+1)^d, d+2),
  * node index C-ordered over the reference coordinates, variables
@@ -143,6 +148,18 @@ int fdg_gate(fdg_mesh_t *mesh, const double *u, void *stream);
 int fdg_reset_status(fdg_mesh_t *mesh, void *stream);
 /* synchronizes `stream`, copies the status record out */
 int fdg_read_status(fdg_mesh_t *mesh, fdg_status_t *out, void *stream);
+
+/* diagnostics reductions over every node of the mesh (rank-local; sums and
+ * the min combine across ranks with an all-reduce).  `a` = u, `b` = dudt
+ * (ENTROPY) or u_exact (ERROR_SQ), else NULL; `out` is a DEVICE buffer of
+ *   CONSERVED: d+2  sum_e,i wbar_i J u[e,i,v]
+ *   ENTROPY:   2    sum wbar J w(u).dudt, sum_e,i,v |wbar J w_v dudt_v|
+ *   ERROR_SQ:  d+2  sum wbar J (u - u_exact)^2
+ *   DT:        1    min J^(1/d) / ((|v| + c)(2p+1))
+ * Deterministic (fixed-order tree, no atomics); no admissibility check
+ * (an inadmissible node gives NaN, as the reference's log/sqrt would). */
+enum fdg_diag { FDG_DIAG_CONSERVED = 0, FDG_DIAG_ENTROPY = 1, FDG_DIAG_ERROR_SQ = 2, FDG_DIAG_DT = 3 };
+int fdg_diagnostic(fdg_mesh_t *mesh, int32_t kind, const double *a, const double *b, double *out, void *stream);
 
 /* halo helper: out[i][m][v] = u[elems[i]][line node m of direction dir at end `side`][v] */
 int fdg_pack_faces(const double *u, const int32_t *elems, int32_t n, int32_t d, int32_t degree, int32_t dir,

@@ -282,3 +282,67 @@ def ssprk43_step(u, dt, rhs_fn):
     u2 = u1 + 0.5 * dt * rhs_fn(u1)
     u3 = (2.0 / 3.0) * u + (1.0 / 3.0) * u2 + (1.0 / 6.0) * dt * rhs_fn(u2)
     return u3 + 0.5 * dt * rhs_fn(u3)
+
+
+# ------------------------------------------------------------ diagnostics
+# numpy restatement of the reference's diagnostics reductions (test
+# infrastructure: checked against tests/golden/diagnostics.npz, written by the
+# reference itself).
+
+
+def _wbar_jac(setup):
+    """wbar (discretization.py:619-621) times J, shape (n_elem, nn)."""
+    wbar = np.ones(1)
+    for _ in range(setup.d):
+        wbar = np.kron(wbar, np.asarray(setup.op.weights, dtype=np.float64))
+    return wbar[None, :] * np.asarray(setup.metrics.jac)
+
+
+def _primitives(u, gamma):
+    d = u.shape[-1] - 2
+    rho = u[..., 0]
+    v = u[..., 1 : d + 1] / rho[..., None]
+    return d, rho, v
+
+
+def entropy_vars(u, gamma):
+    """euler.py:129-146."""
+    d, rho, v = _primitives(u, gamma)
+    p = (gamma - 1.0) * (u[..., d + 1] - 0.5 * rho * np.sum(v * v, axis=-1))
+    s = np.log(p) - gamma * np.log(rho)
+    rho_p = rho / p
+    w = np.empty_like(u)
+    w[..., 0] = (gamma - s) * (1.0 / (gamma - 1.0)) - 0.5 * rho_p * np.sum(v * v, axis=-1)
+    w[..., 1 : d + 1] = rho_p[..., None] * v
+    w[..., d + 1] = -rho_p
+    return w
+
+
+def conserved_totals(u, setup):
+    """discretization.py:1027-1031."""
+    return np.sum(_wbar_jac(setup)[..., None] * u, axis=(0, 1))
+
+
+def entropy_rate(u, dudt, setup, gamma=1.4):
+    """discretization.py:1011-1024: (total, total / scale)."""
+    w = entropy_vars(u, gamma)
+    wt = _wbar_jac(setup)
+    total = float(np.sum(wt * np.sum(w * dudt, axis=-1)))
+    scale = np.sum(np.abs(wt[..., None] * w * dudt))
+    return (0.0, 0.0) if scale == 0.0 else (total, total / scale)
+
+
+def error_norm_l2(u, u_exact, setup):
+    """discretization.py:1033-1037."""
+    diff = u - u_exact
+    return np.sqrt(np.sum(_wbar_jac(setup)[..., None] * diff * diff, axis=(0, 1)))
+
+
+def stable_dt(u, setup, cfl=0.5, gamma=1.4):
+    """timeint.py:138-146 with max_signal_speed (euler.py:105-112)."""
+    d, rho, v = _primitives(u, gamma)
+    mom = u[..., 1 : d + 1]
+    p = (gamma - 1.0) * (u[..., d + 1] - 0.5 * np.sum(mom * mom, axis=-1) / rho)
+    lam = np.sqrt(np.sum(v * v, axis=-1)) + np.sqrt(gamma * p / rho)
+    scale = np.asarray(setup.metrics.jac) ** (1.0 / d)
+    return cfl * float(np.min(scale / (lam * (2 * setup.op.degree + 1))))

@@ -129,6 +129,7 @@ def lib():
     L.fdg_gate.argtypes = [vp, vp, vp]
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]
+    L.fdg_diagnostic.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]
     L.fdg_fp64_probe.argtypes = [P(ctypes.c_double), vp]
     if L.fdg_abi_version() != 1:

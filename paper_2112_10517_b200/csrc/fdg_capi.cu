@@ -7,6 +7,7 @@
 
 #include "../../include/fdg.h"
 #include "fdg_aux.cuh"
+#include "fdg_diag.h"
 #include "fdg_dispatch.cuh"
 
 using namespace fdg;
@@ -21,6 +22,9 @@ struct fdg_mesh {
     KParams base{};
     Status* status = nullptr;       // device
     Status* status_host = nullptr;  // page-locked read-back slot (a pageable D2H target is a slow, bounced copy)
+    double w1d[8] = {};             // 1D LGL weights (diagnostics)
+    double* diag_part = nullptr;    // (diag_blocks, kDiagQ) partials, allocated on first use
+    int diag_blocks = 0;
     // host-buffer pipeline (fdg_volume_host): two copy streams + events, made on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_start = nullptr, ev_done = nullptr;
@@ -115,6 +119,7 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     for (int n = 0; n < 3; ++n)
         for (int i = 0; i < m->p1 * m->p1; ++i)
             k.wts[n][i] = desc->cartesian ? desc->dsplit[i] * desc->areas[n] : desc->dsplit[i];
+    for (int i = 0; i < m->p1; ++i) m->w1d[i] = desc->weights[i];
     k.w0 = desc->weights[0];
     k.wp = desc->weights[m->p1 - 1];
     for (int i = 0; i < 3; ++i) k.areas[i] = desc->areas[i];
@@ -157,6 +162,7 @@ void fdg_mesh_destroy(fdg_mesh_t* m)
     if (!m) return;
     if (m->status) cudaFree(m->status);
     if (m->status_host) cudaFreeHost(m->status_host);
+    if (m->diag_part) cudaFree(m->diag_part);
     if (m->s_in) cudaStreamDestroy(m->s_in);
     if (m->s_out) cudaStreamDestroy(m->s_out);
     for (cudaEvent_t e : {m->ev_start, m->ev_done})
@@ -428,6 +434,43 @@ int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "gate kernel launch");
     g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_diagnostic(fdg_mesh_t* m, int32_t kind, const double* a, const double* b, double* out, void* stream)
+{
+    if (!m || !a || !out) return fail(FDG_ERR_ARG, "fdg_diagnostic: null argument");
+    if (diag_n_out(kind, m->d) == 0) return fail(FDG_ERR_ARG, "fdg_diagnostic: unknown kind %d", kind);
+    if ((kind == FDG_DIAG_ENTROPY || kind == FDG_DIAG_ERROR_SQ) && !b)
+        return fail(FDG_ERR_ARG, "fdg_diagnostic: kind %d needs a second state", kind);
+    if (!m->diag_part) {
+        // one resident wave: kDiagCtasPerSm CTAs of 256 threads per SM
+        m->diag_blocks = kDiagCtasPerSm * m->sm_count;
+        cudaError_t err = cudaMalloc(&m->diag_part, sizeof(double) * kDiagQ * m->diag_blocks);
+        if (err != cudaSuccess) {
+            m->diag_part = nullptr;
+            return cuda_fail(err, "cudaMalloc(diagnostic partials)");
+        }
+    }
+    DiagArgs g;
+    g.d = m->d;
+    g.p1 = m->p1;
+    g.kind = kind;
+    g.n_elem = m->n_elem;
+    g.a = a;
+    g.b = b;
+    g.jac = m->curved ? m->base.jac : nullptr;
+    g.jac_const = m->base.jac_const;
+    for (int i = 0; i < 8; ++i) g.w[i] = m->w1d[i];
+    g.gamma = m->base.gas.gamma;
+    g.gm1 = m->base.gas.gm1;
+    g.igm1 = m->base.gas.igm1;
+    g.part = m->diag_part;
+    g.out = out;
+    g.blocks = m->diag_blocks;
+    cudaError_t err = launch_diagnostic(g, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "diagnostic kernel launch");
+    g_launches.fetch_add(2);
     return FDG_OK;
 }
 

@@ -58,6 +58,10 @@ def _metric_scalars(metrics, d):
     return tuple(areas), float(jac_const)
 
 
+# enum fdg_diag (include/fdg.h)
+DIAG_CONSERVED, DIAG_ENTROPY, DIAG_ERROR_SQ, DIAG_DT = 0, 1, 2, 3
+
+
 class DeviceMesh:
     """Uploaded tables + the libfdg mesh handle for one (partition of a) mesh.
 
@@ -241,6 +245,19 @@ class DeviceMesh:
         rec = N.StatusRec()
         N.check(N.lib().fdg_read_status(self.handle, ctypes.byref(rec), _stream_handle(stream)))
         return int(rec.first_bad), int(rec.bad_stage)
+
+    def diagnostic(self, kind, a, b=None, out=None, stream=None):
+        """fdg_diagnostic: the rank-local reduction `kind` (DIAG_*) of device
+        state(s) into a small device tensor (see include/fdg.h)."""
+        n_out = {DIAG_CONSERVED: self.nvar, DIAG_ENTROPY: 2, DIAG_ERROR_SQ: self.nvar, DIAG_DT: 1}[kind]
+        if out is None:
+            out = self.torch.empty(n_out, dtype=self.torch.float64, device=self.device)
+        N.check(
+            N.lib().fdg_diagnostic(
+                self.handle, int(kind), _ptr(a), None if b is None else _ptr(b), _ptr(out), _stream_handle(stream)
+            )
+        )
+        return out
 
     def pack_faces(self, u, elems, direction, side, out, stream=None):
         N.check(

@@ -26,7 +26,6 @@ import numpy as np
 from . import fluxes as _fluxes
 from .device import device_mesh_for, scheme_struct
 from .errors import AdmissibilityError, ConfigurationError, UnsupportedOperatorError
-from .euler import entropy_vars
 from .geometry import compute_metrics, element_coords, neighbor_table
 from .operators import build_dsplit, node_lines, pair_table
 
@@ -154,7 +153,9 @@ class _Io:
     """Moves a caller's array to the device and the result back in the
     caller's flavour (numpy -> numpy, torch CPU -> torch CPU, CUDA -> CUDA)."""
 
-    def __init__(self, dm, u):
+    def __init__(self, dm, u, key="in"):
+        # `key`: the pinned staging slot; two live _Io objects need two slots
+        # (the first's H2D copy is asynchronous from its slot)
         torch = dm.torch
         self.dm = dm
         self.kind = "cuda" if (_is_torch(u) and u.is_cuda) else ("torch" if _is_torch(u) else "numpy")
@@ -168,7 +169,7 @@ class _Io:
             arr = u if _is_torch(u) else torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
             if tuple(arr.shape) != dm.shape:
                 raise ValueError("state shape %r does not match the mesh %r" % (tuple(arr.shape), dm.shape))
-            pinned = dm.staging("in", dm.shape)
+            pinned = dm.staging(key, dm.shape)
             pinned.copy_(arr)
             self.u = torch.empty(dm.shape, dtype=torch.float64, device=dm.device)
             self.u.copy_(pinned, non_blocking=True)
@@ -297,7 +298,7 @@ def mesh_surface(u, setup, surface_flux, out, kernel="batched"):
         raise ConfigurationError("surface_flux: unknown kind %r" % (surface_flux,))
     dm = device_mesh_for(setup)
     io = _Io(dm, u)
-    acc = _Io(dm, out)
+    acc = _Io(dm, out, key="in2")
     dm.surface(io.u, scheme_struct(None, surface_flux, "none", kernel), acc.u)
     _count(None, _surface_counts(setup), 0)
     return acc.finish(acc.u, out=out)
@@ -375,24 +376,45 @@ def volume_fluxdiff(u_elem, dop, metrics, vol_flux, gas, pre=None):
 # ------------------------------------------------------------- diagnostics
 
 
+def _diag(setup, kind, u, b=None, gate=False):
+    """One fdg_diagnostic reduction on the device; numpy / CPU inputs are
+    copied in. ``gate``: the reference's entropy_vars / max_signal_speed raise
+    on an inadmissible node (euler.py:26-41), so run the device gate first."""
+    dm = device_mesh_for(setup)
+    io = _Io(dm, u)
+    iob = None if b is None else _Io(dm, b, key="in2")
+    if gate:
+        dm.reset_status()
+        dm.gate(io.u)
+    res = dm.diagnostic(kind, io.u, None if iob is None else iob.u)
+    if gate:
+        first_bad, _ = dm.read_status()
+        if first_bad >= 0:
+            dm.raise_if_inadmissible(io.u, first_bad, setup.gas.gamma)
+    return res.cpu().numpy()
+
+
 def entropy_rate(u, dudt, setup):
-    """Normalized semidiscrete entropy production (discretization.py:1011-1024)."""
-    w = entropy_vars(u, setup.gas)
-    weights = setup.wbar[None, :] * setup.metrics.jac
-    contrib = weights * np.sum(w * dudt, axis=-1)
-    scale = np.sum(np.abs(weights[..., None] * w * dudt))
-    total = float(np.sum(contrib))
+    """Normalized semidiscrete entropy production (discretization.py:1011-1024):
+    (sum wbar J w.dudt, that / sum |wbar J w dudt|), both sums on the device."""
+    from .device import DIAG_ENTROPY
+
+    total, scale = (float(x) for x in _diag(setup, DIAG_ENTROPY, u, dudt, gate=True))
     if scale == 0.0:
         return 0.0, 0.0
     return total, total / scale
 
 
 def conserved_totals(u, setup):
-    weights = setup.wbar[None, :] * setup.metrics.jac
-    return np.sum(weights[..., None] * u, axis=(0, 1))
+    """sum wbar J u per variable (discretization.py:1027-1031), on the device."""
+    from .device import DIAG_CONSERVED
+
+    return _diag(setup, DIAG_CONSERVED, u)
 
 
 def error_norm_l2(u, u_exact, setup):
-    weights = setup.wbar[None, :] * setup.metrics.jac
-    diff = u - u_exact
-    return np.sqrt(np.sum(weights[..., None] * diff * diff, axis=(0, 1)))
+    """sqrt(sum wbar J (u - u_exact)^2) per variable (discretization.py:1033-1037);
+    the sums on the device."""
+    from .device import DIAG_ERROR_SQ
+
+    return np.sqrt(_diag(setup, DIAG_ERROR_SQ, u, u_exact))

@@ -131,3 +131,16 @@ class HaloExchange:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
         return self.ghost
+
+
+def combine_diagnostic(kind, local, dist, group=None):
+    """Rank-local fdg_diagnostic results -> the global value, in place: an
+    all-reduce SUM for the sums (CONSERVED, ENTROPY, ERROR_SQ) and MIN for DT,
+    the only global collectives of a sharded run besides the halo
+    (SURVEY.md 8e). ``local`` is the (small) tensor DeviceMesh.diagnostic
+    returned on this rank's slab."""
+    from .device import DIAG_DT
+
+    op = dist.ReduceOp.MIN if kind == DIAG_DT else dist.ReduceOp.SUM
+    dist.all_reduce(local, op=op, group=group)
+    return local

@@ -166,8 +166,18 @@ class StepController:
             raise ConfigurationError("cfl: must be positive, got %r" % (self.cfl,))
 
 
-def stable_dt(u, mesh, metrics, gas, p, controller):
-    """dt = cfl min J^(1/d) / (lambda_max (2p+1))  (reference timeint.py:138-146)."""
+def stable_dt(u, mesh, metrics, gas, p, controller, setup=None):
+    """dt = cfl min J^(1/d) / (lambda_max (2p+1))  (reference timeint.py:138-146).
+
+    ``setup`` (extension): the SpatialSetup ``u`` lives on; with it (required
+    for a CUDA tensor ``u``) the min runs on the device (fdg_diagnostic DT)."""
+    if setup is not None or (hasattr(u, "is_cuda") and u.is_cuda):
+        if setup is None:
+            raise ConfigurationError("stable_dt: a CUDA state needs setup= (the device mesh)")
+        from .device import DIAG_DT
+        from .discretization import _diag
+
+        return controller.cfl * float(_diag(setup, DIAG_DT, u, gate=True)[0])
     lam = max_signal_speed(u, gas)
     scale = np.asarray(metrics.jac) ** (1.0 / mesh.d)
     return controller.cfl * float(np.min(scale / (lam * (2 * p + 1))))

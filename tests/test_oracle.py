@@ -130,3 +130,41 @@ def test_logmean_known_values():
         assert oracle.inv_logmean(a, a) == 1.0 / a
     # well separated: (b - a)/log(b/a)
     assert oracle.logmean(1.0, np.e) == pytest.approx(np.e - 1.0, rel=1e-15)
+
+
+# ------------------------------------------------------------ diagnostics
+
+
+def _diag_golden():
+    return dict(np.load(G.os.path.join(G.GOLDEN, "diagnostics.npz")))
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_diagnostics_oracle_pinned(name):
+    """The numpy restatement of conserved_totals / entropy_rate /
+    error_norm_l2 / stable_dt against the reference's own outputs
+    (tests/golden/make_diagnostics.py). Bar: <= 1e-14 relative (sums),
+    entropy total within 1e-14 of its absolute scale."""
+    g = _diag_golden()
+    c = G.case(name)
+    setup = G.golden_setup(name)
+    for s in G.states(name):
+        u = c["u_" + s]
+        want = g["cons_%s_%s" % (name, s)]
+        got = oracle.conserved_totals(u, setup)
+        assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max(), s
+        assert abs(oracle.stable_dt(u, setup) - float(g["dt_%s_%s" % (name, s)])) <= 1e-15 * float(
+            g["dt_%s_%s" % (name, s)]
+        ), s
+        for vf, sf in (("ranocha", "ranocha"), ("ranocha", "llf")):
+            key = "ent_%s_%s_%s_%s" % (name, s, vf, sf)
+            if key not in g:
+                continue
+            total, norm = oracle.entropy_rate(u, c["rhs_%s_%s_%s" % (s, vf, sf)], setup)
+            t_ref, n_ref = g[key]
+            scale = abs(t_ref / n_ref) if n_ref != 0.0 else 0.0
+            assert abs(total - t_ref) <= 1e-14 * max(scale, 1e-300), key
+    u_exact = c["u_wave"] if "u_wave" in c else 1.01 * c["u_rand"]
+    want = g["err_%s" % name]
+    got = oracle.error_norm_l2(c["u_rand"], u_exact, setup)
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()

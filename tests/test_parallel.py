@@ -101,3 +101,56 @@ def test_partition_tables():
     assert single["n_ghost"] == 0 and np.all(single["plus"] >= 0)
     with pytest.raises(ConfigurationError):
         slab_partition(setup, 0, 5)
+
+
+def _diag_worker(rank, world, port, results):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_2112_10517_b200 import workloads
+    from paper_2112_10517_b200.device import DIAG_CONSERVED, DIAG_DT
+    from paper_2112_10517_b200.parallel import combine_diagnostic, slab_partition
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        setup, u, _ = workloads.build(4, dims=(6, 4, 4))
+        part = slab_partition(setup, rank, world)
+        lo, hi = part["lo"], part["hi"]
+        wj = oracle._wbar_jac(setup)[lo:hi]
+        local = torch.as_tensor(np.sum(wj[..., None] * u[lo:hi], axis=(0, 1)))
+        combine_diagnostic(DIAG_CONSERVED, local, dist)
+        # DT stand-in: this slab's own min of the per-node quotient
+        sub = type("S", (), {})()
+        sub.metrics = type("M", (), {"jac": np.asarray(setup.metrics.jac)[lo:hi]})()
+        sub.op = setup.op
+        dt_local = torch.tensor([oracle.stable_dt(u[lo:hi], sub, cfl=1.0)], dtype=torch.float64)
+        combine_diagnostic(DIAG_DT, dt_local, dist)
+        results[rank] = (local.numpy().copy(), float(dt_local[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_combine_diagnostic(world):
+    """Sharded diagnostics: per-slab partial sums and mins all-reduced with
+    gloo equal the single-domain values (sums within the sequential-sum bound
+    n eps of the absolute sum, the dt min exactly)."""
+    import torch.multiprocessing as mp
+
+    from oracle import oracle
+    from paper_2112_10517_b200 import workloads
+
+    results = mp.Manager().dict()
+    mp.spawn(_diag_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    setup, u, _ = workloads.build(4, dims=(6, 4, 4))
+    terms = oracle._wbar_jac(setup)[..., None] * u
+    want = terms.sum(axis=(0, 1))
+    dt = oracle.stable_dt(u, setup, cfl=1.0)
+    for r in range(world):
+        got, got_dt = results[r]
+        n = terms.shape[0] * terms.shape[1]
+        assert np.all(np.abs(got - want) <= n * 2.3e-16 * np.abs(terms).sum(axis=(0, 1)))
+        assert got_dt == dt
