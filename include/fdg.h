@@ -15,6 +15,7 @@
  *                    (and of SSPRK43, which the reference does not ship)
  *   fdg_gate      <- discretization._admissibility_gate                  discretization.py:660-672
  *   fdg_mesh_create <- the device image of build_setup's SpatialSetup    discretization.py:609-657
+ *   fdg_build_geometry <- geometry.element_coords + compute_metrics       geometry.py:142-178, 200-250
  *   fdg_diagnostic  <- discretization.conserved_totals                   discretization.py:1027-1031
  *                      discretization.entropy_rate (its two sums)        discretization.py:1011-1024
  *                      discretization.error_norm_l2 (before the sqrt)     discretization.py:1033-1037
@@ -160,6 +161,22 @@ int fdg_read_status(fdg_mesh_t *mesh, fdg_status_t *out, void *stream);
  * (an inadmissible node gives NaN, as the reference's log/sqrt would). */
 enum fdg_diag { FDG_DIAG_CONSERVED = 0, FDG_DIAG_ENTROPY = 1, FDG_DIAG_ERROR_SQ = 2, FDG_DIAG_DT = 3 };
 int fdg_diagnostic(fdg_mesh_t *mesh, int32_t kind, const double *a, const double *b, double *out, void *stream);
+
+/* on-device geometry of the periodic box [lo, hi]^d split into dims
+ * elements, warped by amplitude prod_j sin(2 pi t_j) (build_mesh/element_coords),
+ * with the curl-form metrics (compute_metrics). Writes DEVICE arrays:
+ * coords (n_elem, nn, d) and/or ja (n_elem, nn, d, d) + jac (n_elem, nn);
+ * any may be NULL (ja and jac together). n_elem = prod dims. */
+typedef struct fdg_geometry_desc {
+    int32_t d;
+    int32_t degree;        /* p, 1..7 */
+    int32_t dims[3];
+    double lo[3], hi[3];
+    double amplitude;
+    const double *nodes;   /* HOST (p+1) op.nodes */
+    const double *dmat;    /* HOST (p+1)^2 op.D, row-major */
+} fdg_geometry_desc_t;
+int fdg_build_geometry(const fdg_geometry_desc_t *desc, double *coords, double *ja, double *jac, void *stream);
 
 /* halo helper: out[i][m][v] = u[elems[i]][line node m of direction dir at end `side`][v] */
 int fdg_pack_faces(const double *u, const int32_t *elems, int32_t n, int32_t d, int32_t degree, int32_t dir,

@@ -48,6 +48,19 @@ class MeshDesc(ctypes.Structure):
     ]
 
 
+class GeometryDesc(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("degree", ctypes.c_int32),
+        ("dims", ctypes.c_int32 * 3),
+        ("lo", ctypes.c_double * 3),
+        ("hi", ctypes.c_double * 3),
+        ("amplitude", ctypes.c_double),
+        ("nodes", ctypes.c_void_p),
+        ("dmat", ctypes.c_void_p),
+    ]
+
+
 class Scheme(ctypes.Structure):
     _fields_ = [
         ("volume_flux", ctypes.c_int32),
@@ -129,6 +142,7 @@ def lib():
     L.fdg_gate.argtypes = [vp, vp, vp]
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]
+    L.fdg_build_geometry.argtypes = [P(GeometryDesc), vp, vp, vp, vp]
     L.fdg_diagnostic.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]
     L.fdg_fp64_probe.argtypes = [P(ctypes.c_double), vp]

@@ -8,6 +8,7 @@
 #include "../../include/fdg.h"
 #include "fdg_aux.cuh"
 #include "fdg_diag.h"
+#include "fdg_setup.h"
 #include "fdg_dispatch.cuh"
 
 using namespace fdg;
@@ -471,6 +472,40 @@ int fdg_diagnostic(fdg_mesh_t* m, int32_t kind, const double* a, const double* b
     cudaError_t err = launch_diagnostic(g, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "diagnostic kernel launch");
     g_launches.fetch_add(2);
+    return FDG_OK;
+}
+
+int fdg_build_geometry(const fdg_geometry_desc_t* desc, double* coords, double* ja, double* jac, void* stream)
+{
+    if (!desc || !desc->nodes || !desc->dmat) return fail(FDG_ERR_ARG, "fdg_build_geometry: null argument");
+    if (desc->d != 2 && desc->d != 3)
+        return fail(FDG_ERR_UNSUPPORTED, "supported dimensions are 2 and 3, got %d", desc->d);
+    if (desc->degree < 1 || desc->degree > 7)
+        return fail(FDG_ERR_UNSUPPORTED, "degree %d outside the device-supported range 1..7", desc->degree);
+    if ((ja == nullptr) != (jac == nullptr)) return fail(FDG_ERR_ARG, "fdg_build_geometry: ja and jac go together");
+    GeomArgs g;
+    g.d = desc->d;
+    g.p1 = desc->degree + 1;
+    g.n_elem = 1;
+    for (int j = 0; j < g.d; ++j) {
+        if (desc->dims[j] < 1) return fail(FDG_ERR_ARG, "fdg_build_geometry: dims[%d] = %d", j, desc->dims[j]);
+        g.dims[j] = desc->dims[j];
+        g.lo[j] = desc->lo[j];
+        g.hi[j] = desc->hi[j];
+        g.n_elem *= desc->dims[j];
+    }
+    g.amplitude = desc->amplitude;
+    for (int k = 0; k < g.p1; ++k) g.nodes[k] = desc->nodes[k];
+    for (int k = 0; k < g.p1 * g.p1; ++k) g.dmat[k] = desc->dmat[k];
+    g.coords = coords;
+    g.ja = ja;
+    g.jac = jac;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t err = launch_geometry(g, sms, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "geometry kernel launch");
+    g_launches.fetch_add(1);
     return FDG_OK;
 }
 

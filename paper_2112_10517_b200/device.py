@@ -118,8 +118,12 @@ class DeviceMesh:
             areas, jac_const = _metric_scalars(metrics, self.d)
             areas = tuple(areas) + (0.0,) * (3 - len(areas))
         else:
-            self.ja = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.ja)[lo:hi]), device=dev)
-            self.jac = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.jac)[lo:hi]), device=dev)
+            if isinstance(metrics.ja, torch.Tensor):  # device-built geometry (build_setup(device=...))
+                self.ja = metrics.ja[lo:hi].to(dev).contiguous()
+                self.jac = metrics.jac[lo:hi].to(dev).contiguous()
+            else:
+                self.ja = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.ja)[lo:hi]), device=dev)
+                self.jac = torch.as_tensor(np.ascontiguousarray(np.asarray(metrics.jac)[lo:hi]), device=dev)
             if ghost_nrm is not None:
                 self.ghost_nrm = torch.as_tensor(np.ascontiguousarray(ghost_nrm, dtype=np.float64), device=dev)
         desc = N.MeshDesc()

@@ -117,14 +117,26 @@ class SpatialSetup:
         return w
 
 
-def build_setup(mesh, op, gas, with_coords=True):
+def build_setup(mesh, op, gas, with_coords=True, device=None):
     """Geometry, connectivity and operator tables (reference discretization.py:609-657).
     ``with_coords=False`` skips the nodal coordinates of Cartesian meshes
-    (3.2 GB at 128^3, N=3) when no initial condition needs them."""
+    (3.2 GB at 128^3, N=3) when no initial condition needs them.
+    ``device`` (extension, e.g. "cuda"): coordinates and curved metrics are
+    computed on the GPU (geometry.device_geometry) and held as CUDA tensors,
+    so no per-node geometry is built on or copied from the host."""
     if op.family != "lgl":
         raise UnsupportedOperatorError("the flux-differencing setup needs LGL operators, got %r" % (op.family,))
-    coords = element_coords(mesh, op) if (with_coords or not mesh.is_cartesian) else None
-    metrics = compute_metrics(mesh, op, coords)
+    if device is not None:
+        from .geometry import MetricData, device_geometry
+
+        coords, ja, jac = device_geometry(mesh, op, device=device, coords=with_coords)
+        if mesh.is_cartesian:
+            metrics = compute_metrics(mesh, op)  # d areas + J, no per-node arrays
+        else:
+            metrics = MetricData(mesh.d, op.n_nodes, mesh.n_elements, False, ja=ja, jac=jac)
+    else:
+        coords = element_coords(mesh, op) if (with_coords or not mesh.is_cartesian) else None
+        metrics = compute_metrics(mesh, op, coords)
     return SpatialSetup(
         mesh=mesh,
         op=op,

@@ -219,6 +219,51 @@ def compute_metrics(mesh, op, coords=None):
     return MetricData(d, p1, n_elem, False, ja=ja, jac=jac)
 
 
+def device_geometry(mesh, op, device="cuda", coords=True, metrics=True):
+    """element_coords and compute_metrics's curved arrays computed on the GPU
+    (fdg_build_geometry): returns (coords, ja, jac) as CUDA float64 tensors
+    (None where not requested; ja/jac None for Cartesian meshes, whose
+    metrics are scalars). Same arithmetic as the host path up to summation
+    order and the device sin (tests/test_gpu_parity.py pins <= 1e-13)."""
+    import ctypes
+
+    import torch
+
+    from . import _native as N
+
+    d = mesh.d
+    p1 = op.n_nodes
+    nn = p1**d
+    n_elem = mesh.n_elements
+    dev = torch.device(device)
+    want_metrics = metrics and not mesh.is_cartesian
+    c = torch.empty((n_elem, nn, d), dtype=torch.float64, device=dev) if coords else None
+    ja = torch.empty((n_elem, nn, d, d), dtype=torch.float64, device=dev) if want_metrics else None
+    jac = torch.empty((n_elem, nn), dtype=torch.float64, device=dev) if want_metrics else None
+    if c is None and ja is None:
+        return None, None, None
+    nodes = np.ascontiguousarray(op.nodes, dtype=np.float64)
+    dmat = np.ascontiguousarray(op.D, dtype=np.float64)
+    desc = N.GeometryDesc()
+    desc.d, desc.degree = d, p1 - 1
+    desc.dims = (ctypes.c_int32 * 3)(*(tuple(mesh.dims) + (1,) * (3 - d)))
+    desc.lo = (ctypes.c_double * 3)(*(tuple(mesh.lo) + (0.0,) * (3 - d)))
+    desc.hi = (ctypes.c_double * 3)(*(tuple(mesh.hi) + (0.0,) * (3 - d)))
+    desc.amplitude = float(mesh.amplitude)
+    desc.nodes, desc.dmat = nodes.ctypes.data, dmat.ctypes.data
+    ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    N.check(N.lib().fdg_build_geometry(ctypes.byref(desc), ptr(c), ptr(ja), ptr(jac), stream))
+    if jac is not None:
+        jmin = float(jac.min())
+        if not jmin > 0.0:
+            flat = int(torch.argmin(jac))
+            raise MeshError(
+                "non-positive Jacobian %r at element %d, node %d (amplitude too large?)" % (jmin, flat // nn, flat % nn)
+            )
+    return c, ja, jac
+
+
 def neighbor_table(mesh):
     """plus_neighbor[n][e]: element across the +n face of e (periodic)."""
     idx = np.arange(mesh.n_elements).reshape(mesh.dims)

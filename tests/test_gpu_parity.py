@@ -564,3 +564,66 @@ def test_surface_accumulates_into_numpy_out():
     got = P.mesh_surface(u, setup, "llf", acc0.copy(), kernel="reference")
     want = oracle.surface(u, setup, "llf", out=acc0.copy(), variant="cr")
     assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- device geometry
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_device_geometry_matches_reference(name):
+    """fdg_build_geometry (build_setup(device="cuda")) against the reference's
+    recorded coordinates and curl-form metrics. Bars: coords <= 1e-15 of
+    max|x|; Ja and J <= 1e-13 of their max norms (summation order of the
+    derivative sums and the device sin differ from numpy's)."""
+    import torch
+
+    P = _pkg()
+    c = G.case(name)
+    dims = tuple(int(x) for x in c["dims"])
+    bounds = tuple(float(x) for x in c["bounds"])
+    mesh = P.build_mesh(dims, bounds=bounds, amplitude=float(c["amplitude"]))
+    op = P.lgl_operator(int(c["p"]))
+    setup = P.build_setup(mesh, op, P.GasParams(1.4), device="cuda")
+    x = setup.coords.cpu().numpy()
+    assert np.abs(x - c["coords"]).max() <= 1e-15 * np.abs(c["coords"]).max()
+    if bool(c["cartesian"]):
+        assert setup.metrics.cartesian
+        return
+    assert isinstance(setup.metrics.ja, torch.Tensor) and setup.metrics.ja.is_cuda
+    ja = setup.metrics.ja.cpu().numpy()
+    jac = setup.metrics.jac.cpu().numpy()
+    assert np.abs(ja - c["ja"]).max() <= 1e-13 * np.abs(c["ja"]).max()
+    assert np.abs(jac - c["jac"]).max() <= 1e-13 * np.abs(c["jac"]).max()
+
+
+def test_device_geometry_rhs_cfg4():
+    """BASELINE cfg4's warped map (24^3 here, N=4, Kennedy-Gruber + Rusanov):
+    the metrics agree to 1e-12 of max|Ja| (curl-form rounding noise), the
+    RHS on the device-built geometry equals the RHS on the host-built one
+    within the RHS bar (1e-12 of max(|VOL|, |du|)), and the device DT /
+    totals agree (1e-13)."""
+    import torch
+
+    P = _pkg()
+    from paper_2112_10517_b200 import workloads
+
+    setup_h, u, cfg = workloads.build(4, dims=(24, 24, 24))
+    setup_d = P.build_setup(setup_h.mesh, setup_h.op, setup_h.gas, device="cuda")
+    assert np.abs(setup_d.coords.cpu().numpy() - setup_h.coords).max() <= 1e-15
+    ja_h = np.asarray(setup_h.metrics.ja)
+    # curl form: each entry is a difference of derivatives of products
+    # (x_l - mean) d x_m, whose rounding noise (~eps per term, both paths)
+    # is ~1e-15 absolute here against entries of 1.7e-3 -> bar 1e-12
+    assert np.abs(setup_d.metrics.ja.cpu().numpy() - ja_h).max() <= 1e-12 * np.abs(ja_h).max()
+    ud = torch.as_tensor(u, device="cuda")
+    du_h = P.rhs(ud, setup_h, cfg).cpu().numpy()
+    du_d = P.rhs(ud, setup_d, cfg).cpu().numpy()
+    vol = P.mesh_fluxdiff_volume(ud, setup_h, cfg).cpu().numpy()
+    assert np.abs(du_d - du_h).max() <= 1e-12 * max(np.abs(vol).max(), np.abs(du_h).max())
+    t_h = P.conserved_totals(ud, setup_h)
+    t_d = P.conserved_totals(ud, setup_d)
+    assert np.all(np.abs(t_d - t_h) <= 1e-13 * np.abs(t_h).max())
+    sc = P.StepController(0.5)
+    dt_h = P.stable_dt(ud, None, None, setup_h.gas, 4, sc, setup=setup_h)
+    dt_d = P.stable_dt(ud, None, None, setup_d.gas, 4, sc, setup=setup_d)
+    assert abs(dt_d - dt_h) <= 1e-13 * dt_h
