@@ -150,6 +150,15 @@ int fdg_reset_status(fdg_mesh_t *mesh, void *stream);
 /* synchronizes `stream`, copies the status record out */
 int fdg_read_status(fdg_mesh_t *mesh, fdg_status_t *out, void *stream);
 
+/* traversal order of the element kernels: row_order (DEVICE, n_rows int32,
+ * a permutation of 0..n_rows-1, n_rows = n_elem / row_len) lists the rows of
+ * row_len consecutive elements in the order CTAs take them; NULL restores
+ * the natural order. Results are unchanged (every element's arithmetic is
+ * independent of the order); meant for states much larger than L2, where
+ * visiting the mesh tile by tile keeps interface neighbours in L2. The
+ * array must outlive the mesh handle or the next call. */
+int fdg_mesh_set_traversal(fdg_mesh_t *mesh, const int32_t *row_order, int64_t row_len);
+
 /* diagnostics reductions over every node of the mesh (rank-local; sums and
  * the min combine across ranks with an all-reduce).  `a` = u, `b` = dudt
  * (ENTROPY) or u_exact (ERROR_SQ), else NULL; `out` is a DEVICE buffer of

@@ -142,6 +142,7 @@ def lib():
     L.fdg_gate.argtypes = [vp, vp, vp]
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]
+    L.fdg_mesh_set_traversal.argtypes = [vp, vp, ctypes.c_int64]
     L.fdg_build_geometry.argtypes = [P(GeometryDesc), vp, vp, vp, vp]
     L.fdg_diagnostic.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]

@@ -256,6 +256,8 @@ static int volume_range(fdg_mesh* m, const fdg_scheme_t* s, LaunchFn fn, const d
     if (k.jac) k.jac += lo * nn;
     k.n_elem = hi - lo;
     k.elem_base += lo;
+    k.row_order = nullptr;  // the row order indexes the whole mesh
+    k.row_len = 0;
     k.epilogue = EPI_VOLUME;
     k.precompute = s->precompute;
     k.surface_flux = F_LLF;
@@ -435,6 +437,22 @@ int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "gate kernel launch");
     g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_mesh_set_traversal(fdg_mesh_t* m, const int32_t* row_order, int64_t row_len)
+{
+    if (!m) return fail(FDG_ERR_ARG, "fdg_mesh_set_traversal: null mesh");
+    if (!row_order) {
+        m->base.row_order = nullptr;
+        m->base.row_len = 0;
+        return FDG_OK;
+    }
+    if (row_len < 1 || m->n_elem % row_len != 0)
+        return fail(FDG_ERR_ARG, "fdg_mesh_set_traversal: row_len %lld does not divide n_elem %lld",
+                    (long long)row_len, m->n_elem);
+    m->base.row_order = row_order;
+    m->base.row_len = row_len;
     return FDG_OK;
 }
 

@@ -62,6 +62,8 @@ struct KParams {
     int precompute;
     int stage_kind;           // 0: low-storage 2N, 1: Shu-Osher convex combination
     int face_prefetch;        // interface epilogues: prefetch neighbour face rows (state >> L2)
+    const int* row_order;     // traversal: element rows (row_len consecutive elements) in tile order, or null
+    long long row_len;
     unsigned int stage_index;
     double sa, sb, sc, dt;    // 2N: a_i, b_i, -, dt ; SO: A, B, C*dt, -
 };
@@ -621,8 +623,21 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     const long long nbatch = (prm.n_elem + EPB - 1) / EPB;
     const int epi = prm.epilogue;
 
+    // traversal order: batch b covers elements [first(b), first(b) + EPB).
+    // With a row order (fdg_mesh_set_traversal) the rows of the element
+    // index space are visited tile by tile, so the +-x / +-y neighbours a
+    // batch's interface terms read are staged by CTAs of the same wave (L2
+    // hits) instead of 16384 elements away; batches never straddle rows.
+    const bool remap = prm.row_order && (prm.row_len % EPB) == 0;
+    auto first = [&](long long b) -> long long {
+        const long long f = b * EPB;
+        if (!remap) return f;
+        const long long r = f / prm.row_len;
+        return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
+    };
+
     for (long long batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-        const long long e0 = batch * EPB;
+        const long long e0 = first(batch);
         const int ne = (int)min((long long)EPB, prm.n_elem - e0);
         const long long base = e0 * NN * NVAR;
         const int count = ne * NN * NVAR;
@@ -638,13 +653,14 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         {
             const long long nb = batch + gridDim.x;
             if (nb < nbatch) {
-                const long long ne2 = min((long long)EPB, prm.n_elem - nb * EPB);
-                const char* p0 = reinterpret_cast<const char*>(prm.u + nb * EPB * NN * NVAR);
+                const long long f2 = first(nb);
+                const long long ne2 = min((long long)EPB, prm.n_elem - f2);
+                const char* p0 = reinterpret_cast<const char*>(prm.u + f2 * NN * NVAR);
                 const int bytes = (int)(ne2 * NN * NVAR * 8);
                 for (int off = tid * 128; off < bytes; off += NT * 128)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + off));
                 if constexpr (CURVED) {
-                    const char* p1 = reinterpret_cast<const char*>(prm.ja + nb * EPB * NN * D * D);
+                    const char* p1 = reinterpret_cast<const char*>(prm.ja + f2 * NN * D * D);
                     const int b1 = (int)(ne2 * NN * D * D * 8);
                     for (int off = tid * 128; off < b1; off += NT * 128)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(p1 + off));

@@ -7,6 +7,7 @@ op.degree, dsplit.matrix, metrics.{cartesian, ja, jac}, plus_neighbor, gas).
 """
 
 import ctypes
+import os
 import weakref
 
 import numpy as np
@@ -143,6 +144,29 @@ class DeviceMesh:
         self._finalizer = weakref.finalize(self, N.lib().fdg_mesh_destroy, handle)
         self.areas, self.jac_const = areas[: self.d], jac_const
         self._staging = {}
+        self.row_order = None
+        self._set_traversal(setup)
+
+    def _set_traversal(self, setup):
+        """Opt-in tile-by-tile traversal (fdg_mesh_set_traversal), env
+        FDG_TILE="tx,ty": rows of dims[2] elements visited in tiles of
+        tx x ty rows so the +-x / +-y interface neighbours are staged by the
+        same wave. Off by default: on cfg5 128^3 RHS it measured 1-3% slower
+        than the natural order with the face-row prefetch
+        (profiles/r01_tuning.md, v13)."""
+        mesh = getattr(setup, "mesh", None)
+        dims = tuple(getattr(mesh, "dims", ()))
+        env = os.environ.get("FDG_TILE")
+        if self.d != 3 or len(dims) != 3 or env in (None, "", "0"):
+            return
+        tx, ty = (int(v) for v in env.split(","))
+        _, n1, n2 = dims
+        n0 = self.n_elem // (n1 * n2)  # planes held here (slab partitions split direction 0)
+        if n0 * n1 * n2 != self.n_elem or n0 % tx or n1 % ty:
+            return
+        r = np.arange(n0 * n1).reshape(n0 // tx, tx, n1 // ty, ty).transpose(0, 2, 1, 3).ravel()
+        self.row_order = self.torch.as_tensor(r.astype(np.int32), device=self.device)
+        N.check(N.lib().fdg_mesh_set_traversal(self.handle, _ptr(self.row_order), n2))
 
     # ------------------------------------------------------------ shapes
     @property
