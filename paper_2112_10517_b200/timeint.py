@@ -325,6 +325,20 @@ class DeviceStepper:
             if bad_stage >= 0:
                 raise DivergenceError("non-finite state after stage %d (t=%.6g, dt=%.3e)" % (st.index, t, dt))
 
+    def stable_dt(self, u, controller, dist=None, group=None):
+        """stable_dt (timeint.py:138-146) of the device state ``u`` of this
+        rank: fdg_diagnostic DT on the device, all-reduced MIN across ranks
+        when ``dist`` is given (parallel.combine_diagnostic); one 8-byte read
+        back."""
+        from .device import DIAG_DT
+
+        local = self.dm.diagnostic(DIAG_DT, u)
+        if dist is not None:
+            from .parallel import combine_diagnostic
+
+            combine_diagnostic(DIAG_DT, local, dist, group=group)
+        return controller.cfl * float(local[0])
+
     # ---- CUDA graph of one whole step (no status reads inside)
     def capture(self, u, dt):
         """Capture one step from the fixed input ``u`` into a CUDA graph."""
