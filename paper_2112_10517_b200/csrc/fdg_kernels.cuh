@@ -98,6 +98,9 @@ constexpr int kFaceUnroll = FDG_FACE_UNROLL;
 #ifndef FDG_FACE_PREFETCH
 #define FDG_FACE_PREFETCH 1  // neighbour face rows into L2 at batch start (interface epilogues)
 #endif
+#ifndef FDG_NB_SMEM
+#define FDG_NB_SMEM 1  // interface neighbour indices read into shared memory at batch start (v13: cfg4 RHS +7.7%, cfg5 RHS +3.4%)
+#endif
 #ifndef FDG_PDL
 #define FDG_PDL 0  // 1: programmatic dependent launch (fdg_dispatch.cuh); measured no gain in a CUDA graph
 #endif
@@ -496,7 +499,8 @@ __device__ __forceinline__ void face_flux(const KParams& prm, const double* ul, 
 // each face once and scatters both ways).
 
 template <int D, int P1, bool CURVED, int MODE>
-__device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, int n, int side, int m, double* f)
+__device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, int n, int side, int m, double* f,
+                                               int nb_pre = 0)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
@@ -508,7 +512,7 @@ __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, 
     double ul[NVAR], ur[NVAR], nrm[D];
     if (side) {
         load_state<D>(prm.u + (e * G::NN + last) * NVAR, ul);
-        const int nb = __ldg(prm.plus + n * prm.n_elem + e);
+        const int nb = FDG_NB_SMEM ? nb_pre : __ldg(prm.plus + n * prm.n_elem + e);
         if (nb >= 0) load_state<D>(prm.u + ((long long)nb * G::NN + first) * NVAR, ur);
         else load_state<D>(prm.ghost_u + ((long long)(-nb - 1) * FN + m) * NVAR, ur);
         if constexpr (CURVED) {
@@ -516,7 +520,7 @@ __device__ __forceinline__ void face_flux_item(const KParams& prm, long long e, 
             for (int j = 0; j < D; ++j) nrm[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
         }
     } else {
-        const int nb = __ldg(prm.minus + n * prm.n_elem + e);
+        const int nb = FDG_NB_SMEM ? nb_pre : __ldg(prm.minus + n * prm.n_elem + e);
         if (nb >= 0) {
             load_state<D>(prm.u + ((long long)nb * G::NN + last) * NVAR, ul);
             if constexpr (CURVED) {
@@ -622,6 +626,9 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     const unsigned vmask = (USED == NT) ? 0xffffffffu : __ballot_sync(0xffffffffu, tid < USED) * (tid < USED);
     const long long nbatch = (prm.n_elem + EPB - 1) / EPB;
     const int epi = prm.epilogue;
+#if FDG_NB_SMEM
+    __shared__ int s_nb[EPB * 2 * D];
+#endif
 
     // traversal order: batch b covers elements [first(b), first(b) + EPB).
     // With a row order (fdg_mesh_set_traversal) the rows of the element
@@ -701,6 +708,16 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                 }
             }
         }
+#endif
+#if FDG_NB_SMEM
+        // the batch's 2D neighbour indices, read now (their latency hides
+        // behind the volume passes) for the interface phase; the previous
+        // batch's readers passed the face phase's last barrier
+        if (epi != EPI_VOLUME)
+            for (int it = tid; it < EPB * 2 * D; it += NT) {
+                const int fel = it / (2 * D), r = it - fel * 2 * D, n = r >> 1, side = r & 1;
+                s_nb[it] = (fel < ne) ? __ldg((side ? prm.plus : prm.minus) + n * prm.n_elem + e0 + fel) : 0;
+            }
 #endif
         if (epi != EPI_SURFACE) {
             // ---- stage: coalesced copy (AoS), then primitives per node (SoA).
@@ -861,7 +878,11 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                     const int fel = it / NI, r = it - fel * NI;
                     const int side = r / G::LINES, mm = r - side * G::LINES;
                     double fl[NVAR];
+#if FDG_NB_SMEM
+                    face_flux_item<D, P1, CURVED, MODE>(prm, e0 + fel, n, side, mm, fl, s_nb[(fel * D + n) * 2 + side]);
+#else
                     face_flux_item<D, P1, CURVED, MODE>(prm, e0 + fel, n, side, mm, fl);
+#endif
                     const int hi = mm / stride, lo = mm - hi * stride;
                     const int node = (hi * P1 + (side ? P1 - 1 : 0)) * stride + lo;
                     const double J = CURVED ? __ldg(prm.jac + (e0 + fel) * NN + node) : prm.jac_const;
