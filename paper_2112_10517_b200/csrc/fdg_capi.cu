@@ -2,6 +2,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -153,6 +154,8 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         for (int i = 0; i < m->d; ++i) nn *= m->p1;
         const double state_bytes = (double)m->n_elem * (double)nn * (m->d + 2) * 8.0;
         k.face_prefetch = state_bytes > 8.0 * 126.0 * 1024 * 1024;  // >> the 126 MB L2
+        // tuning override (A/B runs only): FDG_FACE_PREFETCH=0|1
+        if (const char* env = getenv("FDG_FACE_PREFETCH")) k.face_prefetch = atoi(env) != 0;
     }
     *out = m;
     return FDG_OK;
