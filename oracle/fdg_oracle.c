@@ -30,7 +30,11 @@
  *
  * Kennedy-Gruber and Chandrashekar (BASELINE cfg 3/4) are not in the
  * reference: their restatement here is "parity unpinned" and is checked by
- * properties only (consistency, symmetry, entropy conservation).
+ * properties only, in tests/test_flux_properties.py: symmetry, consistency
+ * f(u,u,n) = sum_j n_j f^j(u), Cartesian-axis == directional, the
+ * Chandrashekar entropy-conservation residual against 50-digit entropy
+ * variables (Ranocha as the control), and the KEP structure
+ * f_rhov - {v} f_rho = p~ n of both.
  *
  * Surface assembly is written per element and per side (each interface flux
  * is evaluated once from each adjacent element with identical arguments), so

@@ -145,7 +145,6 @@ def mesh_from_setup(setup, lo=0, hi=None):
     weights = np.asarray(setup.op.weights)
     p1 = weights.shape[0]
     metrics = setup.metrics
-    n_elem = metrics.jac.shape[0] if hasattr(metrics, "jac") and metrics.jac is not None else None
     plus = np.stack([np.asarray(setup.plus_neighbor[n]) for n in range(d)])
     n_elem = plus.shape[1]
     minus = np.empty_like(plus)
@@ -153,10 +152,15 @@ def mesh_from_setup(setup, lo=0, hi=None):
         minus[n, plus[n]] = np.arange(n_elem)
     cart = bool(metrics.cartesian)
     ja = None if cart else np.asarray(metrics.ja)
-    jac = np.asarray(metrics.jac) if getattr(metrics, "jac", None) is not None else None
+    jac = None if cart else np.asarray(metrics.jac)
     if cart:
-        areas = np.diag(np.asarray(metrics.ja[0, 0])).copy()
-        jac_const = float(metrics.jac[0, 0])
+        if getattr(metrics, "areas", None) is not None and getattr(metrics, "jac_const", None) is not None:
+            # scalar Cartesian metrics (no per-node arrays materialised)
+            areas = np.asarray(metrics.areas, dtype=np.float64)
+            jac_const = float(metrics.jac_const)
+        else:
+            areas = np.diag(np.asarray(metrics.ja[0, 0])).copy()
+            jac_const = float(metrics.jac[0, 0])
         jac = None
     else:
         areas = None

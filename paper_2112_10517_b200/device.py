@@ -316,7 +316,10 @@ _CACHE = {}
 
 
 def device_mesh_for(setup, device=None):
-    """DeviceMesh cached per setup object (weakly; rebuilt if the setup dies)."""
+    """DeviceMesh cached per setup object. The entry is dropped as soon as the
+    setup is garbage collected (weakref.finalize), which releases the device
+    tables and the libfdg handle with it; objects without weakref support
+    keep their entry (and themselves) alive until ``clear_cache()``."""
     key = (id(setup), str(device))
     hit = _CACHE.get(key)
     if hit is not None and hit[0]() is setup:
@@ -324,10 +327,22 @@ def device_mesh_for(setup, device=None):
     dm = DeviceMesh(setup, device=device)
     try:
         ref = weakref.ref(setup)
+        weakref.finalize(setup, _evict, key, ref)
     except TypeError:  # objects without weakref support: keep them alive with the cache entry
         ref = (lambda s: (lambda: s))(setup)
     _CACHE[key] = (ref, dm)
     return dm
+
+
+def _evict(key, ref):
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is ref:
+        del _CACHE[key]
+
+
+def clear_cache():
+    """Drop every cached DeviceMesh (their device memory is freed once unreferenced)."""
+    _CACHE.clear()
 
 
 __all__ = ["DeviceMesh", "device_mesh_for", "scheme_struct", "DivergenceError"]

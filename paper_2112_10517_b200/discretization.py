@@ -79,6 +79,22 @@ class RhsConfig:
         return scheme_struct(self.volume_flux, self.surface_flux, self.precompute, self.kernel)
 
 
+def as_rhs_config(config):
+    """This package's RhsConfig for ``config``, which may be the reference's
+    own ``fluxdg.RhsConfig`` (discretization.py:87-150) or any object with
+    its fields: the scheme is built from the fields, never from methods the
+    reference's class lacks."""
+    if isinstance(config, RhsConfig):
+        return config
+    try:
+        fields = {k: getattr(config, k) for k in ("volume_scheme", "volume_flux", "surface_flux", "precompute")}
+    except AttributeError as err:
+        raise ConfigurationError("config: not an RhsConfig (%s)" % (err,)) from err
+    fields["kernel"] = getattr(config, "kernel", "reference")
+    fields["overint_degree"] = getattr(config, "overint_degree", None)
+    return RhsConfig(**fields)
+
+
 @dataclass(frozen=True)
 class SpatialSetup:
     """Everything precomputable for RHS evaluations on one mesh/operator
@@ -248,6 +264,12 @@ def _volume_counts(setup, vol_flux):
     return two_point, logmean
 
 
+def _surface_logmeans(surface_flux, n_faces):
+    """Two log means per Ranocha surface evaluation (fluxes.py:281,
+    batched.py:218); Chandrashekar's two (rho and beta) are counted alike."""
+    return 2 * n_faces if surface_flux in ("ranocha", "chandrashekar") else 0
+
+
 def _surface_counts(setup):
     d = setup.d
     p1 = setup.op.degree + 1
@@ -270,32 +292,56 @@ def _raise_gate(dm, io, gas):
 # ------------------------------------------------------------ entry points
 
 
+def _raise_cons2prim(dm, u_dev, gas):
+    """The reference's cons2prim error (euler.py:47-60 via _require_admissible)
+    for a state the device gate rejected."""
+    t = u_dev
+    rho = t[..., 0]
+    mom = t[..., 1 : dm.d + 1]
+    p = (gas.gamma - 1.0) * (t[..., dm.d + 1] - 0.5 * rho * ((mom / rho[..., None]) ** 2).sum(-1))
+    raise AdmissibilityError(
+        "cons2prim: inadmissible state (min rho=%r, min p=%r)" % (float(rho.min()), float(p.min()))
+    )
+
+
 def mesh_fluxdiff_volume(u, setup, config, out=None):
     """VOL = (1/J) sum_n sum_k Dsplit f*_n  for every element (batched.py:450-511).
     Not negated. Raises AdmissibilityError like the reference's cons2prim.
     ``out`` (extension): a CUDA or pinned CPU tensor to receive VOL."""
+    config = as_rhs_config(config)
     config.validate(setup)
     dm = device_mesh_for(setup)
+    scheme = config.scheme()
     if _pinned_f64(u, dm.shape) and (out is None or _pinned_f64(out, dm.shape)):
         # host-resident state: chunked H2D / kernel / D2H pipeline
         dm.reset_status()
         dest = out if out is not None else dm.staging("out", dm.shape)
-        u_dev, res = dm.volume_host(u, config.scheme(), dest)
+        u_dev, res = dm.volume_host(u, scheme, dest)
         io = None
+    elif isinstance(u, np.ndarray) and out is None and u.dtype == np.float64 and u.flags.c_contiguous \
+            and tuple(u.shape) == dm.shape and u.nbytes >= _HOST_PIPELINE_MIN_BYTES:
+        # numpy in / numpy out (the reference's own call): the state goes
+        # through the same chunked pipeline via the pinned staging buffers
+        # (one host memcpy in, one out; the H2D / kernel / D2H chunks overlap)
+        pin_in = dm.staging("in", dm.shape)
+        pin_out = dm.staging("out", dm.shape)
+        np.copyto(pin_in.numpy(), u)
+        dm.reset_status()
+        u_dev, _ = dm.volume_host(pin_in, scheme, pin_out)
+        first_bad, _ = dm.read_status()
+        if first_bad >= 0:
+            _raise_cons2prim(dm, u_dev, setup.gas)
+        tp, lm = _volume_counts(setup, config.volume_flux)
+        _count(None, tp, lm)
+        return pin_out.numpy().copy()
     else:
         io = _Io(dm, u)
         dm.reset_status()
-        res = dm.volume(io.u, config.scheme(), out=io.device_out(out))
+        res = dm.volume(io.u, scheme, out=io.device_out(out))
         u_dev = io.u
     first_bad, _ = dm.read_status()
     if first_bad >= 0:
-        t = u_dev
-        rho = t[..., 0]
-        mom = t[..., 1 : dm.d + 1]
-        p = (setup.gas.gamma - 1.0) * (t[..., dm.d + 1] - 0.5 * rho * ((mom / rho[..., None]) ** 2).sum(-1))
-        raise AdmissibilityError(
-            "cons2prim: inadmissible state (min rho=%r, min p=%r)" % (float(rho.min()), float(p.min()))
-        )
+        _raise_cons2prim(dm, u_dev, setup.gas)
     tp, lm = _volume_counts(setup, config.volume_flux)
     _count(None, tp, lm)
     if io is None:
@@ -304,21 +350,40 @@ def mesh_fluxdiff_volume(u, setup, config, out=None):
     return io.finish(res, out=out)
 
 
+# numpy states at least this large take the chunked host pipeline
+_HOST_PIPELINE_MIN_BYTES = 4 << 20
+
+
 def mesh_surface(u, setup, surface_flux, out, kernel="batched"):
-    """out += SURF, the LGL interface terms (batched.py:514-544)."""
+    """out += SURF, the LGL interface terms (batched.py:514-544). Raises
+    AdmissibilityError like the reference's cons2prim (batched.py:521) on an
+    inadmissible state, before ``out`` is touched."""
     if surface_flux not in SURFACE_KINDS:
         raise ConfigurationError("surface_flux: unknown kind %r" % (surface_flux,))
     dm = device_mesh_for(setup)
     io = _Io(dm, u)
+    dm.reset_status()
+    dm.gate(io.u)
+    first_bad, _ = dm.read_status()
+    if first_bad >= 0:
+        _raise_cons2prim(dm, io.u, setup.gas)
     acc = _Io(dm, out, key="in2")
     dm.surface(io.u, scheme_struct(None, surface_flux, "none", kernel), acc.u)
-    _count(None, _surface_counts(setup), 0)
+    sc = _surface_counts(setup)
+    _count(None, sc, _surface_logmeans(surface_flux, sc))
     return acc.finish(acc.u, out=out)
 
 
-def surface_terms(u, setup, surface_flux, out=None):
+def surface_terms(u, setup, surface_flux, subtract_own=False, face_states=None, out=None):
     """SURF added into ``out`` (zeros if None) with the scalar path's
-    arithmetic (discretization.py:681-760, LGL branch)."""
+    arithmetic (discretization.py:681-760, LGL branch). The reference's
+    strong-form (``subtract_own``) and projected-face (``face_states``)
+    variants serve schemes that are not flux differencing on LGL nodes; they
+    raise UnsupportedOperatorError here."""
+    if subtract_own:
+        raise UnsupportedOperatorError("surface_terms: subtract_own (strong-form coupling) is not on the device path")
+    if face_states is not None:
+        raise UnsupportedOperatorError("surface_terms: face_states overrides are not on the device path")
     if out is None:
         out = np.zeros_like(np.asarray(u, dtype=np.float64)) if not _is_torch(u) else u.new_zeros(u.shape)
     return mesh_surface(u, setup, surface_flux, out, kernel="reference")
@@ -327,6 +392,7 @@ def surface_terms(u, setup, surface_flux, out=None):
 def rhs(u, setup, config, counter=None):
     """du/dt = -(VOL + SURF) (discretization.py:896-949), admissibility gate
     included (discretization.py:660-672)."""
+    config = as_rhs_config(config)
     config.validate(setup)
     dm = device_mesh_for(setup)
     io = _Io(dm, u)
@@ -334,29 +400,53 @@ def rhs(u, setup, config, counter=None):
     res = dm.rhs(io.u, config.scheme(), out=io.device_out())
     _raise_gate(dm, io, setup.gas)
     tp, lm = _volume_counts(setup, config.volume_flux)
-    _count(counter, tp + _surface_counts(setup), lm)
+    sc = _surface_counts(setup)
+    _count(counter, tp + sc, lm + _surface_logmeans(config.surface_flux, sc))
     return io.finish(res)
 
 
 class _ElementSetup:
-    """A one-element periodic setup wrapping per-element metric terms."""
+    """A one-element periodic setup for the per-element entry point. Curved
+    metrics live in device buffers that each call overwrites in place (the
+    DeviceMesh reads them through its pointers), so one device image serves
+    every element of a mesh."""
 
-    def __init__(self, dop, metrics, gas, d):
+    def __init__(self, dop, gas, d, cart):
         from types import SimpleNamespace
 
         self.d = d
         self.op = dop.op
         self.dsplit = dop
         self.gas = gas
-        ja = np.asarray(metrics.ja)
-        jac = np.asarray(metrics.jac)
-        cart = _axis_aligned_areas(ja)
-        if cart is not None:
-            self.metrics = SimpleNamespace(cartesian=True, areas=tuple(cart), jac_const=float(jac[0]), ja=ja[None], jac=jac[None])
-        else:
-            self.metrics = SimpleNamespace(cartesian=False, ja=ja[None], jac=jac[None])
+        nn = dop.op.n_nodes**d
         self.plus_neighbor = tuple(np.zeros(1, dtype=np.int64) for _ in range(d))
         self.n_elements = 1
+        if cart is not None:
+            areas, jac_const = cart
+            self.metrics = SimpleNamespace(cartesian=True, areas=tuple(areas), jac_const=float(jac_const))
+        else:
+            import torch
+
+            self.metrics = SimpleNamespace(
+                cartesian=False,
+                ja=torch.zeros((1, nn, d, d), dtype=torch.float64, device="cuda"),
+                jac=torch.ones((1, nn), dtype=torch.float64, device="cuda"),
+            )
+
+
+_ELEM_CACHE = {}  # key -> (dop, _ElementSetup): strong refs, a few entries (LRU)
+_ELEM_CACHE_MAX = 8
+
+
+def _element_setup(dop, gas, d, cart):
+    key = (id(dop), d, float(gas.gamma), cart)
+    hit = _ELEM_CACHE.pop(key, None)
+    if hit is None or hit[0] is not dop:
+        hit = (dop, _ElementSetup(dop, gas, d, cart))
+    _ELEM_CACHE[key] = hit  # most recent last
+    while len(_ELEM_CACHE) > _ELEM_CACHE_MAX:
+        _ELEM_CACHE.pop(next(iter(_ELEM_CACHE)))
+    return hit[1]
 
 
 def _axis_aligned_areas(ja):
@@ -374,13 +464,26 @@ def volume_fluxdiff(u_elem, dop, metrics, vol_flux, gas, pre=None):
     """One element's VOL with the scalar path's arithmetic
     (discretization.py:267-323). ``pre`` selects the precompute variant like
     the reference's PrecomputedElementData (its ``mode`` is used; the tables
-    themselves are recomputed on the device)."""
+    themselves are recomputed on the device). The device image of the
+    one-element mesh is cached per (dop, gas, Cartesian areas), so a loop over
+    a mesh's elements builds it once."""
     _fluxes.require_volume_kind(vol_flux)
     u_elem = np.asarray(u_elem, dtype=np.float64)
     d = u_elem.shape[-1] - 2
     mode = "none" if pre is None else getattr(pre, "mode", pre)
-    es = _ElementSetup(dop, metrics, gas, d)
-    # cache the one-element device image on the dop object's id
+    ja = np.asarray(metrics.ja, dtype=np.float64)
+    jac = np.asarray(metrics.jac, dtype=np.float64)
+    areas = _axis_aligned_areas(ja)
+    cart = None
+    if areas is not None and np.ptp(jac) == 0.0:
+        cart = (tuple(areas), float(jac[0]))
+    es = _element_setup(dop, gas, d, cart)
+    if cart is None:
+        import torch
+
+        dm = device_mesh_for(es)
+        dm.ja.copy_(torch.from_numpy(np.ascontiguousarray(ja)).view(dm.ja.shape), non_blocking=False)
+        dm.jac.copy_(torch.from_numpy(np.ascontiguousarray(jac)).view(dm.jac.shape), non_blocking=False)
     cfg = RhsConfig(volume_flux=vol_flux, precompute=mode, kernel="reference")
     return mesh_fluxdiff_volume(u_elem[None], es, cfg)[0]
 

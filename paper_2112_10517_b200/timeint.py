@@ -260,17 +260,24 @@ class DeviceStepper:
     ``dm`` is a DeviceMesh, ``config`` an RhsConfig. ``exchange`` (optional)
     is called as ``exchange(v_in) -> ghost_u`` before every stage (halo
     exchange of a slab partition, parallel.py). The state passed to ``step``
-    is never written; the result lives in one of two internal buffers.
+    is never written; the result lives in one of the internal stage buffers.
+    Chained stepping (``u = st.step(u, dt)``) is supported: when ``u`` is one
+    of the stage buffers, the stages ping-pong between the two others (a
+    third buffer is allocated on first need), so no stage overwrites its own
+    input or the Shu-Osher base state u_n.
     """
 
     def __init__(self, dm, config, method=RK54, exchange=None):
+        from .discretization import as_rhs_config
+
+        config = as_rhs_config(config)
         config.validate()
         self.dm = dm
         self.torch = dm.torch
         self.scheme = config.scheme()
         self.method = method
         self.exchange = exchange
-        self.buf = (dm.empty(), dm.empty())
+        self.buf = [dm.empty(), dm.empty()]
         self.reg = dm.empty() if isinstance(method, RKMethod) else None
         self.graph = None
         self._graph_key = None
@@ -280,8 +287,9 @@ class DeviceStepper:
         out = []
         m = self.method
         src = u
+        pool = self._pool(u)
         for i in range(m.n_stages):
-            dst = self.buf[i % 2]
+            dst = pool[i % 2]
             st = N.Stage()
             st.index = i
             st.dt = dt
@@ -293,6 +301,15 @@ class DeviceStepper:
                 out.append((st, src, dst, u if m.A[i] != 0.0 else None))
             src = dst
         return out
+
+    def _pool(self, u):
+        """The two stage buffers of a step from ``u``: never ``u``'s own."""
+        ptr = u.data_ptr() if hasattr(u, "data_ptr") else None
+        free = [b for b in self.buf if b.data_ptr() != ptr]
+        if len(free) < 2:
+            self.buf.append(self.dm.empty())
+            free.append(self.buf[-1])
+        return free[:2]
 
     def _launch(self, stages):
         for st, v_in, v_out, u0 in stages:
@@ -332,6 +349,14 @@ class DeviceStepper:
         back."""
         from .device import DIAG_DT
 
+        # the reference's max_signal_speed raises on an inadmissible node
+        # (euler.py:26-41): gate this rank's slab before anything is reduced,
+        # so a NaN never enters the MIN all-reduce
+        self.dm.reset_status()
+        self.dm.gate(u)
+        first_bad, _ = self.dm.read_status()
+        if first_bad >= 0:
+            self.dm.raise_if_inadmissible(u, first_bad, self.dm.gamma)
         local = self.dm.diagnostic(DIAG_DT, u)
         if dist is not None:
             from .parallel import combine_diagnostic

@@ -23,6 +23,11 @@ What is recorded (all float64, bitwise as the reference produced them):
 * cfg<k>.npz      -- BASELINE.json configs at full size: sampled-element
                      scalar VOL + state/geometry of those elements, and
                      full-mesh checksums of the batched VOL (with --big).
+* cfg4_rhs.npz    -- (--only cfg4rhs) the reference's batched rhs / VOL /
+                     SURF on the full 48^3 curved cfg4 mesh: sampled rows
+                     plus whole-mesh maxima
+* cfg5.npz        -- (--only cfg5) 128^3 noisy-wave elements and their
+                     scalar volume_fluxdiff (Ranocha, Shima)
 """
 
 import argparse
@@ -304,6 +309,75 @@ def make_cfg4():
     print("cfg4 done", flush=True)
 
 
+def make_cfg4_rhs():
+    """cfg4 at full size through the reference's batched rhs (ranocha + llf):
+    du, VOL and SURF on the cfg4 sample elements plus whole-mesh maxima (the
+    scales of the cancellation-aware bar) and checksums. ~35 s, ~20 GB."""
+    mesh = build_mesh((48, 48, 48), bounds=(-1.0, 1.0), amplitude=-0.1)
+    setup = build_setup(mesh, lgl_operator(4), GAS)
+    u = wave_field(setup)
+    idx = sample_elements(setup.n_elements, 12, 4)
+    cfg = RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="batched")
+    t0 = time.time()
+    du = rhs(u, setup, cfg)
+    vol = B.mesh_fluxdiff_volume(u, setup, cfg)
+    surf = B.mesh_surface(u, setup, "llf", np.zeros_like(u))
+    rec = {
+        "elements": idx,
+        "u_sample": u[idx],
+        "du_sample": du[idx],
+        "vol_sample": vol[idx],
+        "surf_sample": surf[idx],
+        "du_max": np.abs(du).max(axis=(0, 1)),
+        "vol_max": np.abs(vol).max(axis=(0, 1)),
+        "surf_max": np.abs(surf).max(axis=(0, 1)),
+        "du_abs_sum": np.abs(du).sum(axis=(0, 1)),
+        "u_sum": u.sum(axis=(0, 1)),
+    }
+    np.savez_compressed(os.path.join(HERE, "cfg4_rhs.npz"), **rec)
+    print("cfg4_rhs done (%.1fs)" % (time.time() - t0), flush=True)
+
+
+def make_cfg5():
+    """cfg5 (128^3, N=3): the BASELINE noisy wave with N(0,1) noise clipped
+    to [-1, 1], coordinates from the reference's
+    element_coords, scalar volume_fluxdiff (Ranocha, Shima) on 16 sampled
+    elements. The full setup (22 GB) is never built: VOL is element-local
+    and the Cartesian metrics are two scalars."""
+    from fluxdg.geometry import MetricTerms, element_coords
+
+    mesh = build_mesh((128, 128, 128), bounds=(-1.0, 1.0))
+    op = lgl_operator(3)
+    coords = element_coords(mesh, op)
+    n_elem, nn = coords.shape[0], coords.shape[1]
+    rng = np.random.default_rng(0)
+    z = np.clip(rng.normal(size=(n_elem, nn)), -1.0, 1.0)
+    idx = sample_elements(n_elem, 16, 5)
+    x = coords[idx]
+    q = np.empty(x.shape[:-1] + (5,))
+    q[..., 0] = 1.0 + 0.98 * np.sin(np.pi * x.sum(-1)) + 0.01 * z[idx]
+    q[..., 1:4] = (0.1, 0.2, 0.3)
+    q[..., 4] = 20.0
+    u = prim2cons(q, GAS)
+    h = 2.0 / 128
+    jac = (0.5 * h) ** 3
+    area = jac / (0.5 * h)
+    ja = np.zeros((nn, 3, 3))
+    for n in range(3):
+        ja[:, n, n] = area
+    terms = MetricTerms(ja, np.full(nn, jac))
+    dop = build_dsplit(op)
+    rec = {"elements": idx, "u_sample": u, "coords_sample": x, "z_sample": z[idx], "jac": np.array(jac),
+           "area": np.array(area)}
+    for flux in ("ranocha", "shima"):
+        rec["vol_%s" % flux] = np.stack([volume_fluxdiff(u[k], dop, terms, flux, GAS, None) for k in range(len(idx))])
+    rec["vol_ranocha_logs"] = np.stack([
+        volume_fluxdiff(u[k], dop, terms, "ranocha", GAS, precompute_element_data(u[k], GAS, "primitives_and_logs"))
+        for k in range(len(idx))])
+    np.savez_compressed(os.path.join(HERE, "cfg5.npz"), **rec)
+    print("cfg5 done", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also write cfg2/cfg3/cfg4 fixtures")
@@ -324,6 +398,10 @@ def main():
             make_cfg3()
         if args.only in (None, "cfg4"):
             make_cfg4()
+    if args.only == "cfg4rhs":
+        make_cfg4_rhs()
+    if args.only == "cfg5":
+        make_cfg5()
 
 
 if __name__ == "__main__":

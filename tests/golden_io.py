@@ -38,7 +38,7 @@ def case(name):
 
 @functools.lru_cache(maxsize=None)
 def config(k):
-    path = os.path.join(GOLDEN, "cfg%d.npz" % k)
+    path = os.path.join(GOLDEN, "cfg%s.npz" % k)
     if not os.path.exists(path):
         return None
     return dict(np.load(path))

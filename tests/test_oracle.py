@@ -168,3 +168,35 @@ def test_diagnostics_oracle_pinned(name):
     want = g["err_%s" % name]
     got = oracle.error_norm_l2(c["u_rand"], u_exact, setup)
     assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+# ---------------------------------------------------- full-size config pins
+
+
+def test_cfg5_sample_oracle_pinned():
+    """The reference's scalar volume_fluxdiff on sampled cfg5 elements
+    (tests/golden/cfg5.npz): the glibc oracle is bitwise equal; the host
+    sample generator (workloads.cartesian_sample, the CPU baseline's input)
+    reproduces the reference's state for element 0 bit for bit."""
+    from types import SimpleNamespace
+
+    from paper_2112_10517_b200 import workloads
+    from paper_2112_10517_b200.euler import GasParams
+    from paper_2112_10517_b200.operators import build_dsplit, lgl_operator
+
+    g = G.config(5)
+    u = g["u_sample"]
+    n = u.shape[0]
+    op = lgl_operator(3)
+    setup = SimpleNamespace(
+        d=3, op=op, dsplit=build_dsplit(op), gas=GasParams(1.4),
+        metrics=SimpleNamespace(cartesian=True, areas=(float(g["area"]),) * 3, jac_const=float(g["jac"])),
+        plus_neighbor=tuple(np.arange(n) for _ in range(3)),
+    )
+    for flux in ("ranocha", "shima"):
+        assert np.array_equal(oracle.volume(u, setup, flux), g["vol_%s" % flux]), flux
+    assert np.array_equal(oracle.volume(u, setup, "ranocha", "primitives_and_logs"), g["vol_ranocha_logs"])
+    assert int(g["elements"][0]) == 0
+    u0, areas, jac = workloads.cartesian_sample(5, 1)
+    assert np.array_equal(u0[0], u[0])
+    assert jac == float(g["jac"]) and areas[0] == float(g["area"])
