@@ -316,10 +316,22 @@ def _gpu_local_cpus(index):
 
 
 def _lib_digest():
-    from paper_2112_10517_b200 import _native as N
-
-    with open(N.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    """sha256 (16 hex) of the kernel SOURCES libfdg.so is built from
+    (csrc/*.cu, *.cuh, *.h, units/, Makefile, include/fdg.h): identifies the
+    build across rebuilds of the same sources."""
+    csrc = os.path.join(ROOT, "paper_2112_10517_b200", "csrc")
+    files = []
+    for base, dirs, names in os.walk(csrc):
+        dirs[:] = sorted(d for d in dirs if not d.startswith("obj"))
+        files += [os.path.join(base, n) for n in names
+                  if n.endswith((".cu", ".cuh", ".h")) or n == "Makefile"]
+    files.append(os.path.join(ROOT, "include", "fdg.h"))
+    h = hashlib.sha256()
+    for f in sorted(files):
+        h.update(os.path.relpath(f, ROOT).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
 
 
 def _traffic_from_profile(workload):
@@ -334,8 +346,8 @@ def _traffic_from_profile(workload):
     ent = rec.get(workload)
     if not ent:
         return None, "no capture of this workload"
-    if ent.get("lib_sha16") != _lib_digest():
-        return None, "capture %s is of another libfdg.so build" % ent.get("capture")
+    if ent.get("src_sha16") != _lib_digest():
+        return None, "capture %s is of another kernel-source revision" % ent.get("capture")
     return ent.get("dram_bytes_per_launch"), ent.get("capture")
 
 
@@ -651,7 +663,7 @@ def run_ours(args, rank, world, local, dist):
         "dtype": "f64",
         "data": "synthetic (seeded BASELINE generators, workloads.build_device)",
         "config": _config_dict(headline, world),
-        "kernel": "FAST element kernel (kernel='batched'), libfdg.so sha256 %s" % _lib_digest(),
+        "kernel": "FAST element kernel (kernel='batched'), libfdg.so kernel-source sha256 %s" % _lib_digest(),
         "timing": r["timing"],
         "roofline": r["roofline"],
         "fp64": r["fp64"],
