@@ -1,9 +1,14 @@
-"""Ideal-gas helpers used on the host (initial conditions, diagnostics).
+"""Ideal-gas state conversions used on the host (initial conditions, error
+reports, diagnostics checks); the device kernels carry their own.
 
-Same conventions as the reference (euler.py:18-75): conserved states carry
-the variable index last, u = (rho, rho v_1..rho v_d, rho E); the arithmetic
-below keeps the reference's operation order so states built here are
-bit-identical to the reference's prim2cons output.
+Contract of the reference's euler module (euler.py:18-146): states carry the
+variable index last, u = (rho, rho v_1..rho v_d, rho E); primitives
+q = (rho, v_1..v_d, p); inadmissible input raises AdmissibilityError with the
+reference's message ("<what>: inadmissible state (min rho=.., min p=..)").
+The floating-point evaluation order of every formula below is the textbook
+one the reference uses too (kinetic energy 1/2 rho |v|^2 with |v|^2 summed in
+component order), so states built here from the same primitives carry the
+same bits (tests/test_setup.py).
 """
 
 from dataclasses import dataclass, field
@@ -15,8 +20,8 @@ from .errors import AdmissibilityError
 
 @dataclass(frozen=True)
 class GasParams:
-    """Ideal gas; 1/(gamma-1) is stored because every energy flux uses it
-    (reference euler.py:18-29)."""
+    """Calorically perfect gas. ``inv_gamma_minus_one`` = 1/(gamma-1) is
+    derived once: every energy flux multiplies by it."""
 
     gamma: float = 1.4
     inv_gamma_minus_one: float = field(init=False)
@@ -27,77 +32,77 @@ class GasParams:
         object.__setattr__(self, "inv_gamma_minus_one", 1.0 / (self.gamma - 1.0))
 
 
-def _dim(u):
-    d = u.shape[-1] - 2
-    if d not in (1, 2, 3):
-        raise AdmissibilityError("state vector length %d is not d+2 for d in 1..3" % u.shape[-1])
-    return d
+def _components(a):
+    """(first, middle d columns, last, d) of a state-like array."""
+    a = np.asarray(a, dtype=float)
+    d = a.shape[-1] - 2
+    if not 1 <= d <= 3:
+        raise AdmissibilityError("state vector length %d is not d+2 for d in 1..3" % a.shape[-1])
+    return a[..., 0], a[..., 1 : d + 1], a[..., d + 1], d
 
 
-def _require_admissible(rho, p, what):
-    if not (np.all(rho > 0.0) and np.all(p > 0.0)):
-        raise AdmissibilityError(
-            "%s: inadmissible state (min rho=%r, min p=%r)" % (what, float(np.min(rho)), float(np.min(p)))
-        )
+def _sq_norm(vec):
+    """|v|^2 summed in component order (v_1^2 + v_2^2) + v_3^2."""
+    acc = vec[..., 0] * vec[..., 0]
+    for i in range(1, vec.shape[-1]):
+        acc = acc + vec[..., i] * vec[..., i]
+    return acc
+
+
+def _check(rho, p, what):
+    if np.all(rho > 0.0) and np.all(p > 0.0):
+        return
+    raise AdmissibilityError(
+        "%s: inadmissible state (min rho=%r, min p=%r)" % (what, float(np.min(rho)), float(np.min(p)))
+    )
+
+
+def _assemble(first, middle, last, like):
+    out = np.empty_like(like)
+    d = middle.shape[-1]
+    out[..., 0] = first
+    out[..., 1 : d + 1] = middle
+    out[..., d + 1] = last
+    return out
 
 
 def prim2cons(q, gas):
-    """(rho, v, p) -> conserved, as reference euler.py:63-75."""
-    q = np.asarray(q, dtype=float)
-    d = _dim(q)
-    rho = q[..., 0]
-    v = q[..., 1 : d + 1]
-    p = q[..., d + 1]
-    _require_admissible(rho, p, "prim2cons")
-    u = np.empty_like(q)
-    u[..., 0] = rho
-    u[..., 1 : d + 1] = rho[..., None] * v
-    u[..., d + 1] = p * gas.inv_gamma_minus_one + 0.5 * rho * np.sum(v * v, axis=-1)
-    return u
+    """(rho, v, p) -> (rho, rho v, rho E), rho E = p/(gamma-1) + 1/2 rho |v|^2."""
+    rho, v, p, _ = _components(q)
+    _check(rho, p, "prim2cons")
+    energy = p * gas.inv_gamma_minus_one + 0.5 * rho * _sq_norm(v)
+    return _assemble(rho, rho[..., None] * v, energy, np.asarray(q, dtype=float))
+
+
+def _velocity_pressure(u, gas):
+    rho, mom, energy, _ = _components(u)
+    v = mom / rho[..., None]
+    p = (gas.gamma - 1.0) * (energy - 0.5 * rho * _sq_norm(v))
+    return rho, v, p
 
 
 def cons2prim(u, gas):
-    """conserved -> (rho, v, p), as reference euler.py:47-60."""
-    u = np.asarray(u, dtype=float)
-    d = _dim(u)
-    rho = u[..., 0]
-    v = u[..., 1 : d + 1] / rho[..., None]
-    kinetic = 0.5 * rho * np.sum(v * v, axis=-1)
-    p = (gas.gamma - 1.0) * (u[..., d + 1] - kinetic)
-    _require_admissible(rho, p, "cons2prim")
-    q = np.empty_like(u)
-    q[..., 0] = rho
-    q[..., 1 : d + 1] = v
-    q[..., d + 1] = p
-    return q
+    """(rho, rho v, rho E) -> (rho, v, p), p = (gamma-1)(rho E - 1/2 rho |v|^2)."""
+    rho, v, p = _velocity_pressure(u, gas)
+    _check(rho, p, "cons2prim")
+    return _assemble(rho, v, p, np.asarray(u, dtype=float))
 
 
 def entropy_vars(u, gas):
-    """Entropy variables for U = -rho s/(gamma-1), s = log p - gamma log rho
-    (reference euler.py:129-146); used by the entropy diagnostics."""
-    u = np.asarray(u, dtype=float)
-    d = _dim(u)
-    rho = u[..., 0]
-    v = u[..., 1 : d + 1] / rho[..., None]
-    p = (gas.gamma - 1.0) * (u[..., d + 1] - 0.5 * rho * np.sum(v * v, axis=-1))
-    _require_admissible(rho, p, "entropy_vars")
+    """w = dU/du for the entropy U = -rho s/(gamma-1), s = log p - gamma log rho:
+    w = ((gamma - s)/(gamma-1) - rho |v|^2/(2p), rho v/p, -rho/p)."""
+    rho, v, p = _velocity_pressure(u, gas)
+    _check(rho, p, "entropy_vars")
     s = np.log(p) - gas.gamma * np.log(rho)
-    rho_p = rho / p
-    w = np.empty_like(u)
-    w[..., 0] = (gas.gamma - s) * gas.inv_gamma_minus_one - 0.5 * rho_p * np.sum(v * v, axis=-1)
-    w[..., 1 : d + 1] = rho_p[..., None] * v
-    w[..., d + 1] = -rho_p
-    return w
+    b = rho / p
+    first = (gas.gamma - s) * gas.inv_gamma_minus_one - 0.5 * b * _sq_norm(v)
+    return _assemble(first, b[..., None] * v, -b, np.asarray(u, dtype=float))
 
 
 def max_signal_speed(u, gas):
-    """|v| + c per node (CFL; reference euler.py:105-112)."""
-    u = np.asarray(u, dtype=float)
-    d = _dim(u)
-    rho = u[..., 0]
-    v = u[..., 1 : d + 1] / rho[..., None]
-    vmag = np.sqrt(np.sum(v * v, axis=-1))
-    mom = u[..., 1 : d + 1]
-    p = (gas.gamma - 1.0) * (u[..., d + 1] - 0.5 * np.sum(mom * mom, axis=-1) / rho)
-    _require_admissible(rho, p, "sound_speed")
-    return vmag + np.sqrt(gas.gamma * p / rho)
+    """|v| + c per node, c = sqrt(gamma p / rho) (the CFL speed)."""
+    rho, mom, energy, _ = _components(u)
+    v = mom / rho[..., None]
+    p = (gas.gamma - 1.0) * (energy - 0.5 * _sq_norm(mom) / rho)
+    _check(rho, p, "sound_speed")
+    return np.sqrt(_sq_norm(v)) + np.sqrt(gas.gamma * p / rho)

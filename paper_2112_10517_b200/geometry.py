@@ -1,14 +1,16 @@
 """Structured periodic box meshes, nodal coordinates and metric terms.
 
-Host-side setup (the device consumes the results once per mesh handle).
-Conventions follow the reference (geometry.py:40-329): element index
-C-ordered over dims, x = lo + L (e + (xi+1)/2)/N per direction, optional
-warp a * prod_j sin(2 pi t_j) added to every coordinate, metric terms
+Host-side setup (the device consumes the results once per mesh handle; for
+large meshes ``device_geometry`` computes the same arrays on the GPU).
+Conventions of the reference (geometry.py:40-329): element index C-ordered
+over dims, x = lo + L (e + (xi+1)/2)/N per direction, optional warp
+a * prod_j sin(2 pi t_j) added to every coordinate, metric terms
 ja[e, i, n, j] = (J a^n)_j by direct differentiation in 2D and the curl form
 in 3D (discrete metric identity to roundoff), face normals taken from the
-minus element's own +face nodes. The numpy call sequence is the reference's,
-so curved metrics are bit-identical to it on the same BLAS
-(tests/test_setup.py).
+minus element's own +face nodes. Coordinates use the reference's mapping
+arithmetic (bitwise equal for equal nodes); the metric derivatives are
+tensor contractions here, equal to the reference's to roundoff
+(tests/test_setup.py: <= 1e-13 relative).
 
 Difference by design: a Cartesian mesh stores its metrics as d areas and one
 Jacobian (the reference materialises per-node arrays, 22 GB at 128^3 N=3);
@@ -68,81 +70,86 @@ def build_mesh(dims, bounds=(-5.0, 5.0), amplitude=0.0):
     return StructuredMesh(dims, lo, hi, float(amplitude))
 
 
-def _element_multi_index(mesh):
-    grids = np.meshgrid(*[np.arange(n) for n in mesh.dims], indexing="ij")
-    return np.stack([g.ravel() for g in grids], axis=-1)
+def _axis_coords(mesh, nodes1d):
+    """Per direction j: (x_j, t_j) on the (dims[j], p+1) grid of element
+    index x node position, t = (e + (xi+1)/2) / n_j the fraction of the box
+    and x = lo_j + L_j t (the mapping of the reference's structured mesh,
+    geometry.py:94-136)."""
+    half = 0.5 * (np.asarray(nodes1d, dtype=np.float64) + 1.0)
+    out = []
+    for j, n in enumerate(mesh.dims):
+        t = (np.arange(n)[:, None] + half[None, :]) / n
+        out.append((mesh.lo[j] + (mesh.hi[j] - mesh.lo[j]) * t, t))
+    return out
 
 
-def _fractions(mesh, nodes1d):
-    half = 0.5 * (nodes1d + 1.0)
-    return [(np.arange(n)[:, None] + half[None, :]) / n for n in mesh.dims]
+def _tensor_grid(per_axis, d, j):
+    """Broadcast direction j's (n_j, p1) table onto the element/node grid
+    (n_0..n_{d-1}, p1, .., p1): axis j is element index, axis d+j node index."""
+    shape = [1] * (2 * d)
+    shape[j] = per_axis.shape[0]
+    shape[d + j] = per_axis.shape[1]
+    return per_axis.reshape(shape)
 
 
 def element_coords(mesh, op):
-    """(n_elements, (p+1)^d, d) nodal coordinates."""
+    """(n_elements, (p+1)^d, d) nodal coordinates: elements C-ordered over
+    dims, nodes C-ordered over the reference axes. A warped mesh adds
+    a * prod_j sin(2 pi t_j) to every coordinate."""
     d = mesh.d
-    tfrac = _fractions(mesh, op.nodes)
-    n1d = tfrac[0].shape[1]
-    elem_idx = _element_multi_index(mesh)
-    n_elem = elem_idx.shape[0]
-    shape = (n1d,) * d
-    nn = n1d**d
-    coords = np.empty((n_elem, nn, d))
-    tgrids = []
+    p1 = len(op.nodes)
+    axes = _axis_coords(mesh, op.nodes)
+    full = tuple(mesh.dims) + (p1,) * d
+    n_elem, nn = mesh.n_elements, p1**d
+    coords = np.empty(full + (d,))
     for j in range(d):
-        t_e = tfrac[j][elem_idx[:, j]]
-        expand = [None] * d
-        expand[j] = slice(None)
-        tgrids.append(np.broadcast_to(t_e[(slice(None),) + tuple(expand)], (n_elem,) + shape))
-    lengths = [b - a for a, b in zip(mesh.lo, mesh.hi)]
-    for j in range(d):
-        coords[:, :, j] = (mesh.lo[j] + lengths[j] * tgrids[j]).reshape(n_elem, nn)
+        coords[..., j] = _tensor_grid(axes[j][0], d, j)
     if mesh.amplitude != 0.0:
-        bump = np.ones((n_elem,) + shape)
-        for j in range(d):
-            bump = bump * np.sin(2.0 * np.pi * tgrids[j])
-        bump = mesh.amplitude * bump.reshape(n_elem, nn)
-        for j in range(d):
-            coords[:, :, j] += bump
-    return coords
+        bump = _tensor_grid(np.sin(2.0 * np.pi * axes[0][1]), d, 0)
+        for j in range(1, d):
+            bump = bump * _tensor_grid(np.sin(2.0 * np.pi * axes[j][1]), d, j)
+        coords += (mesh.amplitude * bump)[..., None]
+    # (e_0..e_{d-1}, a_0..a_{d-1}) is already (element, node) C-order
+    return coords.reshape(n_elem, nn, d)
 
 
-def apply_along(mat, arr, axis):
-    moved = np.moveaxis(arr, axis, -1)
-    return np.moveaxis(moved @ mat.T, -1, axis)
+def _ref_derivative(dmat, f, axis):
+    """d f / d xi_axis of nodal values f (n_elem, p1, .., p1): the 1D
+    differentiation matrix contracted with node axis ``axis`` (0-based over
+    the reference directions)."""
+    return np.moveaxis(np.tensordot(f, dmat, axes=([axis + 1], [1])), -1, axis + 1)
 
 
 def _metrics_2d(x_nd, dmat):
-    x1, x2 = x_nd[..., 0], x_nd[..., 1]
-    d1x1 = apply_along(dmat, x1, 1)
-    d1x2 = apply_along(dmat, x2, 1)
-    d2x1 = apply_along(dmat, x1, 2)
-    d2x2 = apply_along(dmat, x2, 2)
-    ja = np.empty(x1.shape + (2, 2))
-    ja[..., 0, 0] = d2x2
-    ja[..., 0, 1] = -d2x1
-    ja[..., 1, 0] = -d1x2
-    ja[..., 1, 1] = d1x1
-    return ja, d1x1 * d2x2 - d2x1 * d1x2
+    """Ja^n_j by differentiating the mapping: Ja^0 = (y_eta, -x_eta),
+    Ja^1 = (-y_xi, x_xi), J = x_xi y_eta - x_eta y_xi."""
+    g = [[_ref_derivative(dmat, x_nd[..., m], i) for m in range(2)] for i in range(2)]  # g[i][m] = dx_m/dxi_i
+    ja = np.stack(
+        [np.stack([g[1][1], -g[1][0]], axis=-1), np.stack([-g[0][1], g[0][0]], axis=-1)], axis=-2
+    )
+    return ja, g[0][0] * g[1][1] - g[1][0] * g[0][1]
 
 
 def _metrics_3d_curl(x_nd, dmat):
-    x = [x_nd[..., m] for m in range(3)]
-    dx = [[apply_along(dmat, x[m], i + 1) for m in range(3)] for i in range(3)]
-    axes = tuple(range(1, x[0].ndim))
-    x = [c - c.mean(axis=axes, keepdims=True) for c in x]  # shift-invariant curl; small products
-    cyc = ((1, 2), (2, 0), (0, 1))
-    ja = np.empty(x[0].shape + (3, 3))
-    for n in range(3):
-        l, m = cyc[n]
-        for i in range(3):
-            j, k = cyc[i]
-            ja[..., i, n] = apply_along(dmat, x[l] * dx[k][m], j + 1) - apply_along(dmat, x[l] * dx[j][m], k + 1)
-    jac = (
-        dx[0][0] * (dx[1][1] * dx[2][2] - dx[1][2] * dx[2][1])
-        - dx[0][1] * (dx[1][0] * dx[2][2] - dx[1][2] * dx[2][0])
-        + dx[0][2] * (dx[1][0] * dx[2][1] - dx[1][1] * dx[2][0])
-    )
+    """Conservative curl form of the 3D metric terms (Kopriva 2006):
+    Ja^i_n = d_j (x_l d_k x_m) - d_k (x_l d_j x_m) with (j, k) the two
+    reference directions after i and (l, m) the two physical components
+    after n, cyclically. The discrete derivatives commute, so the discrete
+    metric identity sum_i d_i Ja^i = 0 holds to roundoff. Coordinates are
+    re-centred per element first (the form is invariant under a shift of
+    x_l; small products lose less to cancellation)."""
+    g = [[_ref_derivative(dmat, x_nd[..., m], i) for m in range(3)] for i in range(3)]  # dx_m/dxi_i
+    xc = [x_nd[..., m] - x_nd[..., m].mean(axis=(1, 2, 3), keepdims=True) for m in range(3)]
+    nxt = lambda q: ((q + 1) % 3, (q + 2) % 3)  # noqa: E731
+    ja = np.empty(x_nd.shape[:-1] + (3, 3))
+    for i in range(3):
+        j, k = nxt(i)
+        for n in range(3):
+            l, m = nxt(n)
+            ja[..., i, n] = _ref_derivative(dmat, xc[l] * g[k][m], j) - _ref_derivative(dmat, xc[l] * g[j][m], k)
+    rows = [np.stack(g[i], axis=-1) for i in range(3)]  # row i = d x / d xi_i
+    c = np.cross(rows[1], rows[2])
+    jac = rows[0][..., 0] * c[..., 0] + rows[0][..., 1] * c[..., 1] + rows[0][..., 2] * c[..., 2]  # triple product
     return ja, jac
 
 
@@ -265,6 +272,13 @@ def device_geometry(mesh, op, device="cuda", coords=True, metrics=True):
 
 
 def neighbor_table(mesh):
-    """plus_neighbor[n][e]: element across the +n face of e (periodic)."""
-    idx = np.arange(mesh.n_elements).reshape(mesh.dims)
-    return tuple(np.roll(idx, -1, axis=n).ravel().copy() for n in range(mesh.d))
+    """plus_neighbor[n][e]: the element across the +n face of e, periodic in
+    every direction (element multi-index e_n -> (e_n + 1) mod dims[n])."""
+    dims = tuple(mesh.dims)
+    idx = np.indices(dims).reshape(len(dims), -1)
+    out = []
+    for n in range(len(dims)):
+        shifted = idx.copy()
+        shifted[n] = (shifted[n] + 1) % dims[n]
+        out.append(np.ravel_multi_index(tuple(shifted), dims))
+    return tuple(out)

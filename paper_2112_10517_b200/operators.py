@@ -1,37 +1,56 @@
-"""Legendre-Gauss-Lobatto SBP operators and the split-derivative matrix.
+"""One-dimensional SBP operators on [-1, 1] and the tables the kernels consume.
 
-Host-side setup only: the device receives Dsplit and the LGL weights once per
-mesh handle. The construction is the textbook one the reference uses
-(operators.py:79-217): Lobatto nodes as the roots of P'_p by Newton's method
-from Chebyshev-Lobatto guesses, weights 2/(p(p+1)P_p^2), the barycentric
-differentiation matrix, and the SBP re-assembly
-D = (skew(M D) + R^T B N R / 2) / w, so that M D + D^T M = R^T B N R holds to
-a few ulps. The arithmetic sequence is kept identical so the tables are
-bit-for-bit those of the reference (tests/test_setup.py pins them against
-tests/golden/operators.npz).
+Interface (names and meaning of the reference's operators module,
+operators.py:29-357): ``Operator1D`` (degree, family, nodes, weights, D,
+boundary_interp), ``FluxDiffOperator`` (matrix = 2D - M^-1 R^T B N R),
+``lgl_operator``/``make_operator``, ``build_dsplit``, ``node_lines``,
+``pair_table``.
+
+Construction (independent of the reference's float Newton iteration and
+float SBP re-assembly): every table is evaluated in 40-digit arithmetic
+(mpmath) and rounded ONCE to double, so each entry is the correctly rounded
+value of the exact operator:
+
+* nodes: Lobatto = +-1 and the roots of P_p'; Gauss = the roots of P_{p+1};
+  Newton on the three-term Legendre recurrence from Chebyshev guesses;
+* weights: Lobatto 2 / (p (p+1) P_p(x)^2), Gauss 2 / ((1-x^2) P'_{p+1}(x)^2);
+* D: the Lagrange-basis derivative at the nodes in barycentric form,
+  D_ij = (lam_j / lam_i) / (x_i - x_j), D_ii = -sum_{j != i} D_ij;
+* R: the Lagrange basis evaluated at -1 / +1 (unit rows for Lobatto);
+* Dsplit (Lobatto only): 2 D - M^-1 R^T B N R, exact zero diagonal.
+
+The exact operators satisfy M D + D^T M = R^T B N R; the rounded tables do
+to one rounding per entry (tests/test_setup.py). The reference's own
+float construction agrees with these tables to <= 1 ulp of each entry
+(tests/test_setup.py pins that against tests/golden/operators.npz); where a
+test needs the reference's exact bits it takes them from the golden tables
+(tests/golden_io.py), and a reference-built SpatialSetup passed to the
+drop-in entry points is used as given (its Dsplit and weights go to the
+device unchanged).
 """
 
 from dataclasses import dataclass
 from functools import lru_cache
 
+import mpmath
 import numpy as np
 
 from .errors import UnsupportedOperatorError
 
 MAX_DEGREE = 15
 DEVICE_MAX_DEGREE = 7
-
-_FACE_SIGNS = np.array([-1.0, 1.0])
+FAMILIES = ("lgl", "gauss")
+_DPS = 40
 
 
 @dataclass(frozen=True)
 class Operator1D:
     degree: int
     family: str
-    nodes: np.ndarray
-    weights: np.ndarray
-    D: np.ndarray
-    boundary_interp: np.ndarray  # rows evaluate at -1 and +1
+    nodes: np.ndarray            # (p+1,)
+    weights: np.ndarray          # (p+1,) diagonal mass matrix
+    D: np.ndarray                # (p+1, p+1) differentiation matrix
+    boundary_interp: np.ndarray  # (2, p+1): evaluation at -1 (row 0) and +1 (row 1)
 
     @property
     def n_nodes(self):
@@ -40,69 +59,119 @@ class Operator1D:
 
 @dataclass(frozen=True)
 class FluxDiffOperator:
-    """2D - M^{-1} R^T B N R (zero diagonal, M-antisymmetric)."""
+    """2D - M^{-1} R^T B N R: zero diagonal, M-antisymmetric off-diagonal."""
 
     matrix: np.ndarray
     op: Operator1D
 
 
-def _legendre(p, x):
-    """P_p(x) and P_p'(x) by the three-term recurrence."""
-    x = np.asarray(x, dtype=float)
-    prev, cur = np.ones_like(x), x.copy()
-    dprev, dcur = np.zeros_like(x), np.ones_like(x)
-    if p == 0:
-        return prev, dprev
-    for n in range(1, p):
-        nxt = ((2 * n + 1) * x * cur - n * prev) / (n + 1)
-        dnxt = dprev + (2 * n + 1) * cur
-        prev, cur = cur, nxt
-        dprev, dcur = dcur, dnxt
-    return cur, dcur
+# ------------------------------------------------------ exact construction
 
 
-def _lobatto(p):
-    if p == 1:
-        return np.array([-1.0, 1.0]), np.array([1.0, 1.0])
-    x = -np.cos(np.pi * np.arange(1, p) / p)
-    for _ in range(100):
-        leg, dleg = _legendre(p, x)
-        ddleg = (2.0 * x * dleg - p * (p + 1) * leg) / (1.0 - x * x)
-        step = dleg / ddleg
-        x -= step
-        if np.max(np.abs(step)) < 1.0e-15:
-            break
-    x = 0.5 * (x - x[::-1])
-    nodes = np.concatenate(([-1.0], x, [1.0]))
-    leg, _ = _legendre(p, nodes)
-    return nodes, 2.0 / (p * (p + 1) * leg * leg)
+def _legendre_mp(n, x):
+    """(P_n(x), P_n'(x)) in mpmath by the recurrence
+    k P_k = (2k-1) x P_{k-1} - (k-1) P_{k-2}, P_k' = P_{k-2}' + (2k-1) P_{k-1}."""
+    p0, p1 = mpmath.mpf(1), x
+    d0, d1 = mpmath.mpf(0), mpmath.mpf(1)
+    if n == 0:
+        return p0, d0
+    for k in range(2, n + 1):
+        p0, p1 = p1, ((2 * k - 1) * x * p1 - (k - 1) * p0) / k
+        d0, d1 = d1, d0 + (2 * k - 1) * p0
+    return p1, d1
 
 
-def _barycentric(nodes):
-    diff = nodes[:, None] - nodes[None, :]
-    np.fill_diagonal(diff, 1.0)
-    return 1.0 / np.prod(diff, axis=1)
+def _newton_roots(f_df, guesses):
+    out = []
+    tol = mpmath.mpf(10) ** (-(_DPS - 5))
+    for x in guesses:
+        x = mpmath.mpf(x)
+        for _ in range(100):
+            f, df = f_df(x)
+            step = f / df
+            x -= step
+            if abs(step) < tol:
+                break
+        out.append(x)
+    return out
 
 
-def _differentiation(nodes):
-    lam = _barycentric(nodes)
-    diff = nodes[:, None] - nodes[None, :]
-    np.fill_diagonal(diff, 1.0)
-    mat = (lam[None, :] / lam[:, None]) / diff
-    np.fill_diagonal(mat, 0.0)
-    np.fill_diagonal(mat, -np.sum(mat, axis=1))
-    return mat
+def _lobatto_mp(p):
+    # interior nodes: zeros of P_p'; (P_p')' from the Legendre ODE
+    # (1 - x^2) P'' = 2 x P' - p (p+1) P
+    def f_df(x):
+        lp, dlp = _legendre_mp(p, x)
+        return dlp, (2 * x * dlp - p * (p + 1) * lp) / (1 - x * x)
+
+    inner = _newton_roots(f_df, [-mpmath.cos(mpmath.pi * k / p) for k in range(1, p)])
+    nodes = [mpmath.mpf(-1)] + inner + [mpmath.mpf(1)]
+    weights = [mpmath.mpf(2) / (p * (p + 1) * _legendre_mp(p, x)[0] ** 2) for x in nodes]
+    return nodes, weights
 
 
-def _interp_row(nodes, lam, y):
-    diff = y - nodes
-    hit = np.nonzero(diff == 0.0)[0]
-    row = np.zeros_like(nodes)
-    if hit.size:
-        row[hit[0]] = 1.0
-        return row
-    c = lam / diff
-    return c / np.sum(c)
+def _gauss_mp(p):
+    n = p + 1
+    guesses = [-mpmath.cos(mpmath.pi * (k + mpmath.mpf(3) / 4) / (n + mpmath.mpf(1) / 2)) for k in range(n)]
+    nodes = _newton_roots(lambda x: _legendre_mp(n, x), guesses)
+    weights = [mpmath.mpf(2) / ((1 - x * x) * _legendre_mp(n, x)[1] ** 2) for x in nodes]
+    return nodes, weights
+
+
+def _lagrange_tables_mp(nodes):
+    """(D, R) of the Lagrange basis on ``nodes`` in mpmath."""
+    n = len(nodes)
+    lam = []
+    for i in range(n):
+        prod = mpmath.mpf(1)
+        for j in range(n):
+            if j != i:
+                prod *= nodes[i] - nodes[j]
+        lam.append(1 / prod)
+    D = [[mpmath.mpf(0)] * n for _ in range(n)]
+    for i in range(n):
+        for j in range(n):
+            if i != j:
+                D[i][j] = (lam[j] / lam[i]) / (nodes[i] - nodes[j])
+        D[i][i] = -mpmath.fsum(D[i][j] for j in range(n) if j != i)
+    R = []
+    for y in (mpmath.mpf(-1), mpmath.mpf(1)):
+        hit = [k for k in range(n) if nodes[k] == y]
+        if hit:
+            R.append([mpmath.mpf(1) if k == hit[0] else mpmath.mpf(0) for k in range(n)])
+        else:
+            c = [lam[k] / (y - nodes[k]) for k in range(n)]
+            s = mpmath.fsum(c)
+            R.append([ck / s for ck in c])
+    return D, R
+
+
+def _to_f64(a):
+    """Round once to double; entries that are zero in exact arithmetic (the
+    middle node of an odd count, interior LGL diagonals of D, the diagonal
+    of Dsplit) come out of the 40-digit evaluation as ~1e-40 residues and are
+    snapped to an exact 0."""
+    flat = [x for row in a for x in row] if isinstance(a[0], list) else list(a)
+    scale = max(abs(x) for x in flat)
+    tiny = scale * mpmath.mpf(10) ** (-(_DPS - 10))
+    snap = lambda x: 0.0 if abs(x) <= tiny else float(x)  # noqa: E731
+    arr = np.array([[snap(x) for x in row] for row in a]) if isinstance(a[0], list) else np.array([snap(x) for x in a])
+    arr.setflags(write=False)
+    return arr
+
+
+@lru_cache(maxsize=None)
+def _exact_tables(p, family):
+    with mpmath.workdps(_DPS):
+        nodes, weights = (_lobatto_mp if family == "lgl" else _gauss_mp)(p)
+        D, R = _lagrange_tables_mp(nodes)
+        dsplit = None
+        if family == "lgl":
+            n = p + 1
+            # 2D - M^-1 R^T B N R: R^T B N R = diag(-1, 0, .., 0, 1) for Lobatto
+            dsplit = [[2 * D[i][j] for j in range(n)] for i in range(n)]
+            dsplit[0][0] += 1 / weights[0]
+            dsplit[p][p] -= 1 / weights[p]
+        return (_to_f64(nodes), _to_f64(weights), _to_f64(D), _to_f64(R), None if dsplit is None else _to_f64(dsplit))
 
 
 def _check_degree(p):
@@ -111,61 +180,72 @@ def _check_degree(p):
 
 
 @lru_cache(maxsize=None)
-def lgl_operator(p):
-    _check_degree(p)
-    nodes, weights = _lobatto(p)
-    mat = _differentiation(nodes)
-    lam = _barycentric(nodes)
-    boundary = np.vstack([_interp_row(nodes, lam, -1.0), _interp_row(nodes, lam, 1.0)])
-    md = weights[:, None] * mat
-    rtbnr = boundary.T @ (_FACE_SIGNS[:, None] * boundary)
-    mat = (0.5 * (md - md.T) + 0.5 * rtbnr) / weights[:, None]
-    for a in (nodes, weights, mat, boundary):
-        a.setflags(write=False)
-    return Operator1D(p, "lgl", nodes, weights, mat, boundary)
-
-
 def make_operator(p, family="lgl"):
-    if family != "lgl":
-        raise UnsupportedOperatorError(
-            "node family %r: the flux-differencing path is LGL-only (diagonal boundary operator)" % (family,)
-        )
-    return lgl_operator(p)
+    """The degree-p operator of node family ``family`` ('lgl' or 'gauss')."""
+    _check_degree(p)
+    if family not in FAMILIES:
+        raise UnsupportedOperatorError("unknown node family %r (choose from %s)" % (family, ", ".join(FAMILIES)))
+    nodes, weights, D, R, _ = _exact_tables(p, family)
+    return Operator1D(p, family, nodes, weights, D, R)
+
+
+def lgl_operator(p):
+    return make_operator(p, "lgl")
+
+
+def gauss_operator(p):
+    return make_operator(p, "gauss")
 
 
 def build_dsplit(op):
     """Split-derivative matrix for two-point volume fluxes (reference
-    operators.py:204-217): 2D - M^{-1} R^T B N R."""
+    operators.py:204-217): 2D - M^{-1} R^T B N R. Operators built here use
+    the correctly rounded table; any other LGL operator object (e.g. the
+    reference's own) gets it from its D and weights, which for unit
+    boundary rows is 2 D with 1/w_0 added at (0, 0) and 1/w_p subtracted at
+    (p, p) -- the same roundings as the reference's matrix expression."""
     if op.family != "lgl":
         raise UnsupportedOperatorError(
             "split derivative requires a diagonal boundary operator (lgl), got %r" % (op.family,)
         )
-    r = op.boundary_interp
-    mat = 2.0 * op.D - (r.T @ (_FACE_SIGNS[:, None] * r)) / op.weights[:, None]
-    mat.setflags(write=False)
+    if isinstance(op, Operator1D) and op is make_operator(op.degree, "lgl"):
+        mat = _exact_tables(op.degree, "lgl")[4]
+    else:
+        D = np.asarray(op.D, dtype=np.float64)
+        w = np.asarray(op.weights, dtype=np.float64)
+        R = np.asarray(op.boundary_interp, dtype=np.float64)
+        bnd = R[1][:, None] * R[1][None, :] - R[0][:, None] * R[0][None, :]
+        mat = 2.0 * D - bnd / w[:, None]
+        mat.setflags(write=False)
     return FluxDiffOperator(mat, op)
+
+
+# ------------------------------------------------------------ index tables
 
 
 @lru_cache(maxsize=None)
 def node_lines(p1, d):
-    """Per direction, the (p1^(d-1), p1) node ids of every 1D line (reference
-    operators.py:248-259): direction 0 is the slowest axis."""
-    idx = np.arange(p1**d).reshape((p1,) * d)
+    """Per direction n, the (p1^(d-1), p1) node ids of the 1D lines of a
+    (p1)^d element: node ids are C-ordered over the d reference axes
+    (direction 0 slowest), so position a on line m of direction n is
+    (m // s * p1 + a) * s + m % s with s = p1^(d-1-n) -- the same formula
+    the device kernels use (Geo::line_node, fdg_kernels.cuh)."""
     out = []
     for n in range(d):
-        lines = np.ascontiguousarray(np.moveaxis(idx, n, -1).reshape(-1, p1))
-        lines.flags.writeable = False
+        s = p1 ** (d - 1 - n)
+        m = np.arange(p1 ** (d - 1))[:, None]
+        a = np.arange(p1)[None, :]
+        lines = ((m // s) * p1 + a) * s + m % s
+        lines.setflags(write=False)
         out.append(lines)
     return tuple(out)
 
 
 def pair_table(mat):
-    """[(a, b, mat[a,b], mat[b,a]) for a < b] without all-zero pairs
-    (reference operators.py:267-290)."""
-    n = mat.shape[0]
-    return tuple(
-        (a, b, float(mat[a, b]), float(mat[b, a]))
-        for a in range(n)
-        for b in range(a + 1, n)
-        if mat[a, b] != 0.0 or mat[b, a] != 0.0
-    )
+    """Upper-triangle scatter list [(a, b, mat[a,b], mat[b,a]) for a < b]
+    with the pairs whose two weights are both zero dropped (the order the
+    reference's pair loops visit, operators.py:267-290)."""
+    m = np.asarray(mat)
+    ia, ib = np.triu_indices(m.shape[0], k=1)
+    keep = (m[ia, ib] != 0.0) | (m[ib, ia] != 0.0)
+    return tuple((int(a), int(b), float(m[a, b]), float(m[b, a])) for a, b in zip(ia[keep], ib[keep]))

@@ -1,24 +1,35 @@
 """Explicit Runge-Kutta time integration, host API and device-resident steppers.
 
-Host API (reference timeint.py:23-220, same names and semantics):
-``RKMethod``, ``RK54`` (Carpenter-Kennedy 5-stage 4th order, 2N storage),
-``rk_step(u, t, dt, rhs_fn, method)``, ``integrate(...)``, ``stable_dt``.
+Host API (the reference's timeint module, timeint.py:23-220: same names,
+arguments, semantics and error messages): ``RKMethod`` (2N-storage
+coefficients a, b, c), ``RK54`` (Carpenter-Kennedy five-stage fourth order),
+``StepController``, ``stable_dt``, ``rk_step(u, t, dt, rhs_fn, method)``,
+``integrate(...)``.
 
 Added (BASELINE config 4; not in the reference, parity unpinned):
-``SSPRK43`` -- the four-stage third-order strong-stability-preserving method
-in Shu-Osher form
+``ShuOsherMethod`` and ``SSPRK43`` -- the four-stage third-order
+strong-stability-preserving method
 
     u1 = u  + dt/2 L(u);   u2 = u1 + dt/2 L(u1)
     u3 = 2/3 u + 1/3 u2 + dt/6 L(u2);   u_new = u3 + dt/2 L(u3)
 
+Validation at construction: every method is reduced to its Butcher tableau
+by running the scheme's update rules on symbolic stage-derivative
+coefficients (a linear simulation), and the tableau is checked against the
+order conditions b . Psi(t) = 1/gamma(t) of every rooted tree t up to the
+method's order (generated recursively), plus c = A 1. A mistyped
+coefficient fails loudly at import.
+
 Device path: ``DeviceStepper`` runs every stage as ONE fused kernel
-(fdg_rk_stage: volume + surface + RHS + stage update, ping-pong state
-buffers), optionally captured in a CUDA graph, and checks the admissibility /
-finiteness status once per step. On a failure it replays the step stage by
-stage to raise exactly the error the reference's rk_step would raise.
+(fdg_rk_stage: volume + surface + RHS + stage update), optionally captured in
+a CUDA graph, and checks the admissibility / finiteness status once per step.
+On a failure it replays the step stage by stage to raise exactly the error
+the reference's rk_step would raise.
 """
 
 from dataclasses import dataclass
+from fractions import Fraction
+from functools import lru_cache
 
 import numpy as np
 
@@ -26,10 +37,101 @@ from . import _native as N
 from .errors import AdmissibilityError, ConfigurationError, DivergenceError
 from .euler import max_signal_speed
 
+# ----------------------------------------------------------- order theory
+
+
+@lru_cache(maxsize=None)
+def _rooted_trees(order):
+    """All rooted trees with ``order`` nodes as sorted tuples of subtrees
+    (the one-node tree is ())."""
+    if order == 1:
+        return ((),)
+    out = set()
+
+    def forests(n, max_tree):
+        # multisets of trees with n nodes in total, trees in non-increasing order
+        if n == 0:
+            yield ()
+            return
+        for k in range(n, 0, -1):
+            for t in _rooted_trees(k):
+                if max_tree is not None and (k, t) > max_tree:
+                    continue
+                for rest in forests(n - k, (k, t)):
+                    yield ((k, t),) + rest
+
+    for f in forests(order - 1, None):
+        out.add(tuple(sorted(t for _, t in f)))
+    return tuple(sorted(out))
+
+
+def _size(tree):
+    return 1 + sum(_size(t) for t in tree)
+
+
+def _density(tree):
+    g = _size(tree)
+    for t in tree:
+        g *= _density(t)
+    return g
+
+
+def _stage_weights(tree, amat):
+    """Psi(t): the per-stage elementary weight vector, Psi(()) = 1 and
+    Psi([t_1..t_m]) = prod_k A Psi(t_k)."""
+    psi = np.ones(amat.shape[0])
+    for t in tree:
+        psi = psi * (amat @ _stage_weights(t, amat))
+    return psi
+
+
+def _validate_tableau(name, amat, bvec, cvec, order, tol=1e-14):
+    residuals = {"stage times": float(np.max(np.abs(amat.sum(axis=1) - cvec)))}
+    for k in range(1, order + 1):
+        for tree in _rooted_trees(k):
+            got = float(bvec @ _stage_weights(tree, amat))
+            residuals["tree %s (order %d)" % (tree, k)] = abs(got - 1.0 / _density(tree))
+    worst = max(residuals, key=residuals.get)
+    if residuals[worst] > tol:
+        raise ConfigurationError("order conditions violated for %r: %s residual %.3e" % (name, worst, residuals[worst]))
+
+
+def _simulate_2n(a, b):
+    """Butcher (A, b) of the 2N scheme du <- a_i du + dt k_i, v <- v + b_i du,
+    by carrying du and v as coefficient vectors over (dt k_0 .. dt k_{s-1})."""
+    s = len(b)
+    amat = np.zeros((s, s))
+    du = np.zeros(s)
+    v = np.zeros(s)
+    for i in range(s):
+        amat[i] = v  # stage i is evaluated at the current v
+        du = a[i] * du
+        du[i] += 1.0
+        v = v + b[i] * du
+    return amat, v
+
+
+def _simulate_shu_osher(A, B, C):
+    """Butcher (A, b) of y_i = A_i u + B_i y_{i-1} + C_i dt L(y_{i-1})."""
+    s = len(C)
+    amat = np.zeros((s, s))
+    y = np.zeros(s)  # y_0 = u: no stage derivative yet
+    for i in range(s):
+        if abs(A[i] + B[i] - 1.0) > 1e-15:
+            raise ConfigurationError("stage %d: A + B must be 1" % (i + 1))
+        amat[i] = y
+        y = B[i] * y  # the A_i u part contributes no stage derivative
+        y[i] += C[i]
+    return amat, y
+
+
+# ------------------------------------------------------------------ methods
+
 
 @dataclass(frozen=True)
 class RKMethod:
-    """Low-storage (2N) coefficients: du <- a_i du + dt f; v <- v + b_i du."""
+    """2N-storage explicit Runge-Kutta coefficients: per stage
+    du <- a_i du + dt f(v, t + c_i dt); v <- v + b_i du."""
 
     name: str
     a: tuple
@@ -44,16 +146,27 @@ class RKMethod:
             )
         if self.a[0] != 0.0:
             raise ConfigurationError("a[0] must be 0 (nothing to carry into the first stage)")
-        _check_order_conditions(*_butcher_2n(self.a, self.b), np.asarray(self.c), self.order, self.name)
+        amat, bvec = _simulate_2n(self.a, self.b)
+        _validate_tableau(self.name, amat, bvec, np.asarray(self.c, dtype=float), self.order)
 
     @property
     def n_stages(self):
         return len(self.b)
 
+    def advance(self, u, t, dt, rhs_fn):
+        du = u * 0.0
+        v = u.copy() if hasattr(u, "copy") else u.clone()
+        for i, (ai, bi, ci) in enumerate(zip(self.a, self.b, self.c)):
+            du = ai * du + dt * rhs_fn(v, t + ci * dt)
+            v = v + bi * du
+            _require_finite(v, i, t, dt)
+        return v
+
 
 @dataclass(frozen=True)
 class ShuOsherMethod:
-    """Stages y_i = A_i u_n + B_i y_{i-1} + C_i dt L(y_{i-1}) (y_0 = u_n)."""
+    """Convex-combination stages y_i = A_i u_n + B_i y_{i-1} + C_i dt L(y_{i-1}),
+    y_0 = u_n (SSP form: A_i, B_i >= 0, A_i + B_i = 1)."""
 
     name: str
     A: tuple
@@ -63,65 +176,30 @@ class ShuOsherMethod:
     order: int = 3
 
     def __post_init__(self):
-        _check_order_conditions(*_butcher_shu_osher(self.A, self.B, self.C), np.asarray(self.c), self.order, self.name)
+        amat, bvec = _simulate_shu_osher(self.A, self.B, self.C)
+        _validate_tableau(self.name, amat, bvec, np.asarray(self.c, dtype=float), self.order)
 
     @property
     def n_stages(self):
         return len(self.C)
 
-
-def _butcher_2n(a, b):
-    """(A, b) of the Butcher tableau implied by a 2N scheme."""
-    s = len(b)
-    rows = []
-    for i in range(1, s + 1):
-        row = []
-        for m in range(i):
-            coef = b[m]
-            prod = 1.0
-            for n in range(m + 1, i):
-                prod *= a[n]
-                coef += b[n] * prod
-            row.append(coef)
-        rows.append(row)
-    amat = np.zeros((s, s))
-    for i in range(1, s):
-        amat[i, : len(rows[i - 1])] = rows[i - 1]
-    return amat, np.asarray(rows[-1], dtype=float)
+    def advance(self, u, t, dt, rhs_fn):
+        y = u
+        for i in range(self.n_stages):
+            k = rhs_fn(y, t + self.c[i] * dt)
+            base = y if self.A[i] == 0.0 else self.A[i] * u + self.B[i] * y
+            y = base + (self.C[i] * dt) * k
+            _require_finite(y, i, t, dt)
+        return y
 
 
-def _butcher_shu_osher(A, B, C):
-    """Butcher (A, b) of y_i = A_i u + B_i y_{i-1} + C_i dt L(y_{i-1})."""
-    s = len(C)
-    # represent each y_i as u + sum_j W[i, j] dt L(y_j)
-    W = np.zeros((s + 1, s))
-    for i in range(1, s + 1):
-        W[i] = B[i - 1] * W[i - 1]
-        W[i, i - 1] += C[i - 1]
-        # A_i + B_i must be 1 for consistency
-        if abs(A[i - 1] + B[i - 1] - 1.0) > 1e-15:
-            raise ConfigurationError("stage %d: A + B must be 1" % i)
-    return W[:s], W[s]
+def _require_finite(v, stage, t, dt):
+    ok = bool(v.isfinite().all()) if hasattr(v, "isfinite") else bool(np.all(np.isfinite(v)))
+    if not ok:
+        raise DivergenceError("non-finite state after stage %d (t=%.6g, dt=%.3e)" % (stage, t, dt))
 
 
-def _check_order_conditions(amat, bw, c, order, name, tol=1e-14):
-    residuals = {"stage times": float(np.max(np.abs(amat.sum(axis=1) - c)))}
-    ac = amat @ c
-    conds = [("sum b", bw.sum(), 1.0), ("b.c", bw @ c, 0.5), ("b.c^2", bw @ c**2, 1 / 3), ("b.Ac", bw @ ac, 1 / 6)]
-    if order >= 4:
-        conds += [
-            ("b.c^3", bw @ c**3, 0.25),
-            ("b.(c*Ac)", bw @ (c * ac), 0.125),
-            ("b.Ac^2", bw @ (amat @ c**2), 1 / 12),
-            ("b.AAc", bw @ (amat @ ac), 1 / 24),
-        ]
-    for label, got, want in conds:
-        residuals[label] = abs(float(got) - want)
-    worst = max(residuals, key=residuals.get)
-    if residuals[worst] > tol:
-        raise ConfigurationError("order conditions violated for %r: %s residual %.3e" % (name, worst, residuals[worst]))
-
-
+# Carpenter & Kennedy (1994), five-stage fourth-order 2N-storage scheme
 RK54 = RKMethod(
     "carpenter-kennedy 5/4",
     a=(
@@ -149,9 +227,9 @@ RK54 = RKMethod(
 
 SSPRK43 = ShuOsherMethod(
     "ssprk(4,3)",
-    A=(0.0, 0.0, 2.0 / 3.0, 0.0),
-    B=(1.0, 1.0, 1.0 / 3.0, 1.0),
-    C=(0.5, 0.5, 1.0 / 6.0, 0.5),
+    A=(0.0, 0.0, float(Fraction(2, 3)), 0.0),
+    B=(1.0, 1.0, float(Fraction(1, 3)), 1.0),
+    C=(0.5, 0.5, float(Fraction(1, 6)), 0.5),
     c=(0.0, 0.5, 1.0, 0.5),
     order=3,
 )
@@ -159,6 +237,8 @@ SSPRK43 = ShuOsherMethod(
 
 @dataclass(frozen=True)
 class StepController:
+    """CFL number of the step-size rule in stable_dt."""
+
     cfl: float = 0.5
 
     def __post_init__(self):
@@ -167,7 +247,9 @@ class StepController:
 
 
 def stable_dt(u, mesh, metrics, gas, p, controller, setup=None):
-    """dt = cfl min J^(1/d) / (lambda_max (2p+1))  (reference timeint.py:138-146).
+    """dt = cfl min_nodes J^(1/d) / (lambda_max (2p+1)) (reference
+    timeint.py:138-146): J^(1/d) the local mesh size, (2p+1) the degree
+    scaling of the explicit limit.
 
     ``setup`` (extension): the SpatialSetup ``u`` lives on; with it (required
     for a CUDA tensor ``u``) the min runs on the device (fdg_diagnostic DT)."""
@@ -178,74 +260,48 @@ def stable_dt(u, mesh, metrics, gas, p, controller, setup=None):
         from .discretization import _diag
 
         return controller.cfl * float(_diag(setup, DIAG_DT, u, gate=True)[0])
-    lam = max_signal_speed(u, gas)
-    scale = np.asarray(metrics.jac) ** (1.0 / mesh.d)
-    return controller.cfl * float(np.min(scale / (lam * (2 * p + 1))))
-
-
-def _isfinite_all(v):
-    if hasattr(v, "isfinite"):
-        return bool(v.isfinite().all())
-    return bool(np.all(np.isfinite(v)))
+    d = len(mesh.dims)
+    h = np.asarray(metrics.jac) ** (1.0 / d)
+    return controller.cfl * float(np.min(h / (max_signal_speed(u, gas) * (2 * p + 1))))
 
 
 def rk_step(u, t, dt, rhs_fn, method=RK54):
-    """One step with any rhs_fn (host API, reference timeint.py:149-163)."""
+    """One step of ``method`` with exactly one rhs_fn(v, t) call per stage;
+    raises DivergenceError on a non-finite stage (reference timeint.py:149-163)."""
     if not dt > 0.0:
         raise ConfigurationError("dt: must be positive, got %r" % (dt,))
-    if isinstance(method, ShuOsherMethod):
-        u0 = u
-        y = u
-        for i in range(method.n_stages):
-            k = rhs_fn(y, t + method.c[i] * dt)
-            if method.A[i] != 0.0:
-                y = method.A[i] * u0 + method.B[i] * y + (method.C[i] * dt) * k
-            else:
-                y = y + (method.C[i] * dt) * k
-            if not _isfinite_all(y):
-                raise DivergenceError("non-finite state after stage %d (t=%.6g, dt=%.3e)" % (i, t, dt))
-        return y
-    du = u * 0.0
-    v = u.copy() if hasattr(u, "copy") else u.clone()
-    for i in range(method.n_stages):
-        k = rhs_fn(v, t + method.c[i] * dt)
-        du = method.a[i] * du + dt * k
-        v = v + method.b[i] * du
-        if not _isfinite_all(v):
-            raise DivergenceError("non-finite state after stage %d (t=%.6g, dt=%.3e)" % (i, t, dt))
-    return v
+    return method.advance(u, t, dt, rhs_fn)
 
 
 def integrate(u0, rhs_fn, *, n_steps=None, t_end=None, dt=None, dt_fn=None, t0=0.0, method=RK54, callbacks=()):
-    """March rhs_fn from u0 (reference timeint.py:166-220)."""
+    """March rhs_fn from u0 for ``n_steps`` steps or up to ``t_end`` (the last
+    step clipped to land on it), with a fixed ``dt`` or ``dt_fn(u, t)``;
+    callbacks run as cb(step, t, dt, u) after every step. A stage
+    DivergenceError is re-raised with the last good state attached
+    (.last_fields, .step, .t). Returns (u, {"steps", "t", "rhs_evals"})
+    (reference timeint.py:166-220)."""
     if (n_steps is None) == (t_end is None):
         raise ConfigurationError("exactly one of n_steps and t_end must be given")
     if (dt is None) == (dt_fn is None):
         raise ConfigurationError("exactly one of dt and dt_fn must be given")
+    slack = 0.0 if t_end is None else 1e-12 * max(1.0, abs(t_end))
+
+    def finished(step, t):
+        return step >= n_steps if n_steps is not None else t >= t_end - slack
+
     u = u0.copy() if hasattr(u0, "copy") else u0.clone()
-    t = t0
-    step = 0
-    eps = 1e-12 * max(1.0, abs(t_end)) if t_end is not None else 0.0
-    while True:
-        if n_steps is not None:
-            if step >= n_steps:
-                break
-        elif t >= t_end - eps:
-            break
+    t, step = t0, 0
+    while not finished(step, t):
         h = dt if dt is not None else dt_fn(u, t)
         if t_end is not None and t + h > t_end:
             h = t_end - t
         try:
-            u_next = rk_step(u, t, h, rhs_fn, method)
+            u_new = rk_step(u, t, h, rhs_fn, method)
         except DivergenceError as err:
             wrapped = DivergenceError("diverged in step %d at t=%.6g: %s" % (step, t, err))
-            wrapped.last_fields = u
-            wrapped.step = step
-            wrapped.t = t
+            wrapped.last_fields, wrapped.step, wrapped.t = u, step, t
             raise wrapped from err
-        u = u_next
-        t += h
-        step += 1
+        u, t, step = u_new, t + h, step + 1
         for cb in callbacks:
             cb(step, t, h, u)
     return u, {"steps": step, "t": t, "rhs_evals": method.n_stages * step}

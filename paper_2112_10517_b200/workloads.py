@@ -66,12 +66,14 @@ def noisy_wave_primitives(coords, seed=0):
     return q
 
 
-def build(k, dims=None, kernel="batched", volume_flux=None, precompute=None):
-    """(setup, u, config) for BASELINE config ``k`` (optionally resized)."""
+def build(k, dims=None, kernel="batched", volume_flux=None, precompute=None, op=None):
+    """(setup, u, config) for BASELINE config ``k`` (optionally resized).
+    ``op``: the 1D operator (default lgl_operator(p); tests pass the
+    reference's recorded tables to reproduce its states bit for bit)."""
     c = CONFIGS[k]
     dims = tuple(dims) if dims is not None else c["dims"]
     mesh = build_mesh(dims, bounds=(-1.0, 1.0), amplitude=c["amplitude"])
-    setup = build_setup(mesh, lgl_operator(c["p"]), GAS)
+    setup = build_setup(mesh, op if op is not None else lgl_operator(c["p"]), GAS)
     if c["state"] == "wave":
         q = wave_primitives(setup.coords)
     elif c["state"] == "random":
@@ -101,7 +103,7 @@ def _prim2cons_torch(q, igm1):
     return u
 
 
-def build_device(k, dims=None, kernel="batched", volume_flux=None, precompute=None, device="cuda"):
+def build_device(k, dims=None, kernel="batched", volume_flux=None, precompute=None, device="cuda", op=None):
     """(setup, u, config) for BASELINE config ``k`` with the geometry built
     on the GPU (build_setup(device=...): fdg_build_geometry) and the state
     computed there from the device coordinates: no per-node host arrays, so
@@ -117,7 +119,7 @@ def build_device(k, dims=None, kernel="batched", volume_flux=None, precompute=No
     c = CONFIGS[k]
     dims = tuple(dims) if dims is not None else c["dims"]
     mesh = build_mesh(dims, bounds=(-1.0, 1.0), amplitude=c["amplitude"])
-    op = lgl_operator(c["p"])
+    op = op if op is not None else lgl_operator(c["p"])
     need_coords = c["state"] != "random"
     setup = build_setup(mesh, op, GAS, with_coords=need_coords, device=device)
     n_elem, nn, d = setup.n_elements, setup.n_nodes, setup.d
@@ -147,7 +149,7 @@ def build_device(k, dims=None, kernel="batched", volume_flux=None, precompute=No
     return setup, u, config
 
 
-def cartesian_sample(k, n_elem_sample, gas=GAS):
+def cartesian_sample(k, n_elem_sample, gas=GAS, op=None):
     """Host state of the first ``n_elem_sample`` elements of Cartesian config
     ``k`` (C-ordered element index), built with the reference's coordinate
     formula (geometry.py:94-136: x = lo + L (e + (xi+1)/2)/n) and the config's
@@ -158,7 +160,7 @@ def cartesian_sample(k, n_elem_sample, gas=GAS):
         raise ValueError("cartesian_sample: config %d is curved" % k)
     dims = c["dims"]
     d = len(dims)
-    op = lgl_operator(c["p"])
+    op = op if op is not None else lgl_operator(c["p"])
     p1 = op.n_nodes
     nn = p1**d
     half = 0.5 * (op.nodes + 1.0)

@@ -44,6 +44,16 @@ def config(k):
     return dict(np.load(path))
 
 
+@functools.lru_cache(maxsize=None)
+def golden_operator(p):
+    """The reference's own lgl_operator(p) tables as an Operator1D (its exact
+    bits, for tests that rebuild reference states or setups bit for bit)."""
+    from paper_2112_10517_b200.operators import Operator1D
+
+    ops = operators()
+    return Operator1D(p, "lgl", ops["nodes_%d" % p], ops["weights_%d" % p], ops["D_%d" % p], ops["R_%d" % p])
+
+
 def golden_setup(name, gamma=1.4):
     """Duck-typed setup built only from the reference's recorded arrays."""
     c = case(name)

@@ -114,7 +114,7 @@ def test_cfg5_reference_sample(flux):
     g = G.config(5)
     u = g["u_sample"]
     n = u.shape[0]
-    op = P.lgl_operator(3)
+    op = G.golden_operator(3)
     area = float(g["area"])
     setup = SimpleNamespace(
         d=3, op=op, dsplit=P.build_dsplit(op), gas=P.GasParams(1.4),
@@ -144,7 +144,7 @@ def test_cfg5_reference_sample(flux):
 def cfg4():
     from paper_2112_10517_b200 import workloads
 
-    setup, u, _ = workloads.build(4, kernel="reference")
+    setup, u, _ = workloads.build(4, kernel="reference", op=G.golden_operator(4))
     return setup, u
 
 

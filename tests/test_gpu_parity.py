@@ -101,7 +101,7 @@ def test_cfg1_faithful_bitwise_and_literal_du():
     from paper_2112_10517_b200 import workloads
 
     g = G.config(1)
-    setup, u, _ = workloads.build(1)
+    setup, u, _ = workloads.build(1, op=G.golden_operator(3))
     du = P.rhs(u, setup, P.RhsConfig(volume_flux="ranocha", surface_flux="llf", kernel="reference"))
     assert np.array_equal(du, oracle.rhs(u, setup, "ranocha", "llf", variant="cr"))
     assert _rel(du, g["du"]) <= 1e-12
@@ -155,7 +155,7 @@ def test_cfg2_samples_and_checksum():
     from paper_2112_10517_b200 import workloads
 
     g = G.config(2)
-    setup, u, _ = workloads.build(2)
+    setup, u, _ = workloads.build(2, op=G.golden_operator(3))
     idx = g["elements"]
     for kernel, pre, key, tol in (
         ("reference", "none", "vol_ranocha", 1e-13),
@@ -174,7 +174,7 @@ def test_cfg4_samples_curved():
     from paper_2112_10517_b200 import workloads
 
     g = G.config(4)
-    setup, u, _ = workloads.build(4)
+    setup, u, _ = workloads.build(4, op=G.golden_operator(4))
     idx = g["elements"]
     for flux in ("ranocha", "shima"):
         ref = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux=flux, kernel="reference"))
@@ -188,7 +188,7 @@ def test_cfg3_samples_n7():
     from paper_2112_10517_b200 import workloads
 
     g = G.config(3)
-    setup, u, _ = workloads.build(3)
+    setup, u, _ = workloads.build(3, op=G.golden_operator(7))
     idx = g["elements"]
     ref = P.mesh_fluxdiff_volume(u, setup, P.RhsConfig(volume_flux="ranocha", kernel="reference"))
     assert _rel(ref[idx], g["vol_ranocha"]) <= 1e-13
@@ -582,7 +582,7 @@ def test_device_geometry_matches_reference(name):
     dims = tuple(int(x) for x in c["dims"])
     bounds = tuple(float(x) for x in c["bounds"])
     mesh = P.build_mesh(dims, bounds=bounds, amplitude=float(c["amplitude"]))
-    op = P.lgl_operator(int(c["p"]))
+    op = G.golden_operator(int(c["p"]))
     setup = P.build_setup(mesh, op, P.GasParams(1.4), device="cuda")
     x = setup.coords.cpu().numpy()
     assert np.abs(x - c["coords"]).max() <= 1e-15 * np.abs(c["coords"]).max()

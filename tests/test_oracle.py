@@ -187,7 +187,7 @@ def test_cfg5_sample_oracle_pinned():
     g = G.config(5)
     u = g["u_sample"]
     n = u.shape[0]
-    op = lgl_operator(3)
+    op = G.golden_operator(3)
     setup = SimpleNamespace(
         d=3, op=op, dsplit=build_dsplit(op), gas=GasParams(1.4),
         metrics=SimpleNamespace(cartesian=True, areas=(float(g["area"]),) * 3, jac_const=float(g["jac"])),
@@ -197,6 +197,6 @@ def test_cfg5_sample_oracle_pinned():
         assert np.array_equal(oracle.volume(u, setup, flux), g["vol_%s" % flux]), flux
     assert np.array_equal(oracle.volume(u, setup, "ranocha", "primitives_and_logs"), g["vol_ranocha_logs"])
     assert int(g["elements"][0]) == 0
-    u0, areas, jac = workloads.cartesian_sample(5, 1)
+    u0, areas, jac = workloads.cartesian_sample(5, 1, op=G.golden_operator(3))
     assert np.array_equal(u0[0], u[0])
     assert jac == float(g["jac"]) and areas[0] == float(g["area"])
