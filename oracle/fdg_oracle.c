@@ -556,23 +556,31 @@ int or_max_threads(void)
     return n > 0 ? (int)n : 1;
 }
 
-static void run_parallel(const or_mesh *M, const double *u, double *out, int flux, int pre,
-                         int what, int nthreads)
+static void run_parallel_range(const or_mesh *M, const double *u, double *out, int flux, int pre,
+                               int what, int64_t lo, int64_t hi, int nthreads)
 {
+    const int64_t n = hi - lo;
+    if (n <= 0) return;
     if (nthreads <= 0) nthreads = or_max_threads();
     if (nthreads > 256) nthreads = 256;
-    if ((int64_t)nthreads > M->n_elem) nthreads = (int)(M->n_elem > 0 ? M->n_elem : 1);
+    if ((int64_t)nthreads > n) nthreads = (int)n;
     job_t jobs[256];
     pthread_t tids[256];
     for (int t = 0; t < nthreads; ++t) {
         jobs[t].M = M; jobs[t].u = u; jobs[t].out = out;
         jobs[t].flux = flux; jobs[t].pre = pre; jobs[t].what = what;
-        jobs[t].lo = M->n_elem * t / nthreads;
-        jobs[t].hi = M->n_elem * (t + 1) / nthreads;
+        jobs[t].lo = lo + n * t / nthreads;
+        jobs[t].hi = lo + n * (t + 1) / nthreads;
     }
     if (nthreads == 1) { run_job(&jobs[0]); return; }
     for (int t = 0; t < nthreads; ++t) pthread_create(&tids[t], NULL, run_job, &jobs[t]);
     for (int t = 0; t < nthreads; ++t) pthread_join(tids[t], NULL);
+}
+
+static void run_parallel(const or_mesh *M, const double *u, double *out, int flux, int pre,
+                         int what, int nthreads)
+{
+    run_parallel_range(M, u, out, flux, pre, what, 0, M->n_elem, nthreads);
 }
 
 /* VOL (already / J), discretization.py:267-323 applied to every element */
@@ -621,6 +629,17 @@ int64_t or_rhs(const or_mesh *M, const double *u, double *du, int vflux, int sfl
     or_surface(M, u, du, sflux, nthreads);
     run_parallel(M, u, du, 0, 0, 2, nthreads);
     return -1;
+}
+
+/* rows [lo, hi) of or_rhs (no gate): the interior / boundary split of a slab
+ * partition -- interior rows never read ghost_u, which may still be NULL    */
+int or_rhs_range(const or_mesh *M, const double *u, double *du, int vflux, int sflux, int pre,
+                 int64_t lo, int64_t hi, int nthreads)
+{
+    run_parallel_range(M, u, du, vflux, pre, 0, lo, hi, nthreads);
+    run_parallel_range(M, u, du, sflux, 0, 1, lo, hi, nthreads);
+    run_parallel_range(M, u, du, 0, 0, 2, lo, hi, nthreads);
+    return 0;
 }
 
 /* single two-point flux evaluation (conserved input), for property tests */

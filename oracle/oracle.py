@@ -94,6 +94,8 @@ def lib(variant="glibc"):
         L.or_surface.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int]
         L.or_rhs.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.or_rhs.restype = ctypes.c_int64
+        L.or_rhs_range.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                   ctypes.c_int64, ctypes.c_int]
         L.or_gate.argtypes = [P, vp, vp, vp]
         L.or_gate.restype = ctypes.c_int64
         L.or_two_point.argtypes = [
@@ -225,6 +227,18 @@ def rhs(u, setup, volume_flux="ranocha", surface_flux="ranocha", precompute="non
         ctypes.byref(m.struct), _ptr(u), _ptr(du), FLUX_IDS[volume_flux], FLUX_IDS[surface_flux],
         PRE_IDS[precompute], nthreads,
     )
+    return du
+
+
+def rhs_range(u, mesh, du, lo, hi, volume_flux="ranocha", surface_flux="ranocha", precompute="none", nthreads=0,
+              variant="glibc"):
+    """Rows [lo, hi) of rhs into ``du`` (no gate): the interior / boundary
+    split of a slab partition (interior rows never read ghost traces)."""
+    m = _mesh(mesh)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    assert du.flags.c_contiguous and du.dtype == np.float64 and du.shape == u.shape
+    lib(variant).or_rhs_range(ctypes.byref(m.struct), _ptr(u), _ptr(du), FLUX_IDS[volume_flux], FLUX_IDS[surface_flux],
+                              PRE_IDS[precompute], int(lo), int(hi), nthreads)
     return du
 
 

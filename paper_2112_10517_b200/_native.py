@@ -99,7 +99,9 @@ EXPORTS = (
     "fdg_volume_host",
     "fdg_surface",
     "fdg_rhs",
+    "fdg_rhs_range",
     "fdg_rk_stage",
+    "fdg_rk_stage_range",
     "fdg_gate",
     "fdg_reset_status",
     "fdg_read_status",
@@ -139,6 +141,8 @@ def lib():
     L.fdg_surface.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rhs.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rk_stage.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, vp]
+    L.fdg_rhs_range.argtypes = [vp, P(Scheme), vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
+    L.fdg_rk_stage_range.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
     L.fdg_gate.argtypes = [vp, vp, vp]
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]

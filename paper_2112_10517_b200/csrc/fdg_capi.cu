@@ -133,6 +133,8 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     k.minus = desc->minus;
     k.ghost_nrm = desc->ghost_nrm;
     k.n_elem = desc->n_elem;
+    k.range_lo = 0;
+    k.range_hi = desc->n_elem;
     k.elem_base = desc->elem_base;
     k.gas.gamma = desc->gamma;
     k.gas.gm1 = desc->gamma - 1.0;  // fluxes.py: gm1 = gas.gamma - 1.0
@@ -258,6 +260,8 @@ static int volume_range(fdg_mesh* m, const fdg_scheme_t* s, LaunchFn fn, const d
     if (k.ja) k.ja += lo * nn * m->d * m->d;
     if (k.jac) k.jac += lo * nn;
     k.n_elem = hi - lo;
+    k.range_lo = 0;
+    k.range_hi = hi - lo;
     k.elem_base += lo;
     k.row_order = nullptr;  // the row order indexes the whole mesh
     k.row_len = 0;
@@ -377,13 +381,23 @@ int fdg_surface(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const dou
     return run(m, s, k, F_SHIMA, stream);
 }
 
-int fdg_rhs(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* du,
-            void* stream)
+static int check_range(const fdg_mesh* m, int64_t lo, int64_t hi, const char* who)
+{
+    if (lo < 0 || hi > m->n_elem || lo > hi)
+        return fail(FDG_ERR_ARG, "%s: bad element range [%lld, %lld) of %lld", who, (long long)lo, (long long)hi,
+                    m->n_elem);
+    return FDG_OK;
+}
+
+int fdg_rhs_range(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* du, int64_t lo,
+                  int64_t hi, void* stream)
 {
     if (!m || !u || !du) return fail(FDG_ERR_ARG, "fdg_rhs: null argument");
     if (u == du) return fail(FDG_ERR_ARG, "fdg_rhs: du must not alias u");
     int rc = check_scheme(s, true, true);
+    if (!rc) rc = check_range(m, lo, hi, "fdg_rhs_range");
     if (rc) return rc;
+    if (lo == hi) return FDG_OK;
     KParams k = m->base;
     k.u = u;
     k.out = du;
@@ -391,11 +405,21 @@ int fdg_rhs(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double*
     k.epilogue = EPI_RHS;
     k.surface_flux = s->surface_flux;
     k.precompute = s->precompute;
+    k.range_lo = lo;
+    k.range_hi = hi;
     return run(m, s, k, s->volume_flux, stream);
 }
 
-int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, const double* v_in,
-                 const double* ghost_u, double* v_out, double* reg, const double* u0, void* stream)
+int fdg_rhs(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* du,
+            void* stream)
+{
+    if (!m) return fail(FDG_ERR_ARG, "fdg_rhs: null argument");
+    return fdg_rhs_range(m, s, u, ghost_u, du, 0, m->n_elem, stream);
+}
+
+int fdg_rk_stage_range(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, const double* v_in,
+                       const double* ghost_u, double* v_out, double* reg, const double* u0, int64_t lo, int64_t hi,
+                       void* stream)
 {
     if (!m || !st || !v_in || !v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: null argument");
     if (v_in == v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: v_out must not alias v_in");
@@ -403,7 +427,9 @@ int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, co
     if (st->kind == 1 && st->a != 0.0 && !u0) return fail(FDG_ERR_ARG, "fdg_rk_stage: stage needs u0");
     if (st->kind != 0 && st->kind != 1) return fail(FDG_ERR_CONFIG, "stage kind %d unknown", st->kind);
     int rc = check_scheme(s, true, true);
+    if (!rc) rc = check_range(m, lo, hi, "fdg_rk_stage_range");
     if (rc) return rc;
+    if (lo == hi) return FDG_OK;
     KParams k = m->base;
     k.u = v_in;
     k.out = v_out;
@@ -419,7 +445,16 @@ int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, co
     k.sb = st->b;
     k.sc = st->cdt;
     k.dt = st->dt;
+    k.range_lo = lo;
+    k.range_hi = hi;
     return run(m, s, k, s->volume_flux, stream);
+}
+
+int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, const double* v_in,
+                 const double* ghost_u, double* v_out, double* reg, const double* u0, void* stream)
+{
+    if (!m) return fail(FDG_ERR_ARG, "fdg_rk_stage: null argument");
+    return fdg_rk_stage_range(m, s, st, v_in, ghost_u, v_out, reg, u0, 0, m->n_elem, stream);
 }
 
 int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)

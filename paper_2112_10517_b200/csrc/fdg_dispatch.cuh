@@ -72,16 +72,28 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
     using G = Geo<D, P1>;
     constexpr size_t smem = (size_t)smem_doubles<D, P1, VF, LOGS>() * sizeof(double);
     constexpr bool twin = has_hiocc<D, P1, MODE, CURVED>();
-    static int bps = -1, bps_hi = -1;  // resident CTAs per SM (one device per process)
-    if (bps < 0) {
+    // resident CTAs per SM, cached per device (a process may drive several)
+    constexpr int kMaxDev = 64;
+    static int bps_tab[kMaxDev] = {}, bps_hi_tab[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int bps = 0, bps_hi = 0;
+    if (dev >= 0 && dev < kMaxDev && bps_tab[dev] > 0) {
+        bps = bps_tab[dev];
+        bps_hi = bps_hi_tab[dev];
+    } else {
         cudaError_t err = elem_occupancy<D, P1, VF, CURVED, MODE, LOGS, 0>(&bps);
         if (err != cudaSuccess) return err;
         if constexpr (twin) {
             err = elem_occupancy<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>(&bps_hi);
             if (err != cudaSuccess) return err;
         }
+        if (dev >= 0 && dev < kMaxDev) {
+            bps_hi_tab[dev] = bps_hi;
+            bps_tab[dev] = bps;  // published last: a reader seeing bps > 0 sees bps_hi
+        }
     }
-    const long long nb = (p.n_elem + G::EPB - 1) / G::EPB;
+    const long long nb = (p.range_hi - p.range_lo + G::EPB - 1) / G::EPB;
     if (nb <= 0) return cudaSuccess;
     const long long slots = (long long)bps * sm_count;
     if constexpr (twin) {

@@ -49,7 +49,9 @@ struct KParams {
     double* reg;              // RK 2N register
     const double* u0;         // Shu-Osher stage base state
     Status* status;
-    long long n_elem;
+    long long n_elem;         // elements of the mesh handle (neighbour-table stride)
+    long long range_lo;       // this launch covers elements [range_lo, range_hi) (interior /
+    long long range_hi;       //   boundary split of a partition); [0, n_elem) by default
     long long elem_base;      // added to element indices reported by the gate
     double wts[3][64];        // per direction: Dsplit[a,b] * Ja^n_n (Cartesian) or Dsplit (curved)
     double areas[3];          // Cartesian Ja^n_n
@@ -624,7 +626,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     // warps -- a compile-time full mask when the CTA has no spare threads
     constexpr int USED = EPB * G::LINES;
     const unsigned vmask = (USED == NT) ? 0xffffffffu : __ballot_sync(0xffffffffu, tid < USED) * (tid < USED);
-    const long long nbatch = (prm.n_elem + EPB - 1) / EPB;
+    const long long nbatch = (prm.range_hi - prm.range_lo + EPB - 1) / EPB;
     const int epi = prm.epilogue;
 #if FDG_NB_SMEM
     __shared__ int s_nb[EPB * 2 * D];
@@ -635,9 +637,9 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     // index space are visited tile by tile, so the +-x / +-y neighbours a
     // batch's interface terms read are staged by CTAs of the same wave (L2
     // hits) instead of 16384 elements away; batches never straddle rows.
-    const bool remap = prm.row_order && (prm.row_len % EPB) == 0;
+    const bool remap = prm.row_order && (prm.row_len % EPB) == 0 && prm.range_lo == 0 && prm.range_hi == prm.n_elem;
     auto first = [&](long long b) -> long long {
-        const long long f = b * EPB;
+        const long long f = prm.range_lo + b * EPB;
         if (!remap) return f;
         const long long r = f / prm.row_len;
         return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
@@ -645,13 +647,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
 
     for (long long batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
         const long long e0 = first(batch);
-        const int ne = (int)min((long long)EPB, prm.n_elem - e0);
+        const int ne = (int)min((long long)EPB, prm.range_hi - e0);
         const long long base = e0 * NN * NVAR;
         const int count = ne * NN * NVAR;
         const long long e = e0 + el;
         const bool active = (el < ne);
-        const bool tma = tma_u && (count % 2) == 0;
-        const bool tma_out = tma_out_ok && (count % 2) == 0;
+        // (a batch starting at an odd double offset -- odd-size elements in a
+        // range launch starting at an odd element -- takes the copy loops)
+        const bool tma = tma_u && (count % 2) == 0 && (base % 2) == 0;
+        const bool tma_out = tma_out_ok && (count % 2) == 0 && (base % 2) == 0;
 
 #if FDG_PREFETCH
         // warm L2 with the next batch of this CTA (its state, and metrics on
@@ -661,7 +665,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             const long long nb = batch + gridDim.x;
             if (nb < nbatch) {
                 const long long f2 = first(nb);
-                const long long ne2 = min((long long)EPB, prm.n_elem - f2);
+                const long long ne2 = min((long long)EPB, prm.range_hi - f2);
                 const char* p0 = reinterpret_cast<const char*>(prm.u + f2 * NN * NVAR);
                 const int bytes = (int)(ne2 * NN * NVAR * 8);
                 for (int off = tid * 128; off < bytes; off += NT * 128)

@@ -240,27 +240,27 @@ class DeviceMesh:
         )
         return out
 
-    def rhs(self, u, scheme, out=None, ghost_u=None, stream=None):
+    def rhs(self, u, scheme, out=None, ghost_u=None, stream=None, lo=None, hi=None):
+        """du = -(VOL + SURF); with ``lo``/``hi`` only the local elements
+        [lo, hi) (fdg_rhs_range: the overlap split of a slab)."""
         out = self.empty() if out is None else out
-        N.check(
-            N.lib().fdg_rhs(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out), _stream_handle(stream))
-        )
+        if lo is None and hi is None:
+            N.check(N.lib().fdg_rhs(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out),
+                                    _stream_handle(stream)))
+        else:
+            N.check(N.lib().fdg_rhs_range(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out),
+                                          int(0 if lo is None else lo), int(self.n_elem if hi is None else hi),
+                                          _stream_handle(stream)))
         return out
 
-    def stage(self, scheme, stage, v_in, v_out, reg=None, u0=None, ghost_u=None, stream=None):
-        N.check(
-            N.lib().fdg_rk_stage(
-                self.handle,
-                ctypes.byref(scheme),
-                ctypes.byref(stage),
-                _ptr(v_in),
-                _ptr(ghost_u),
-                _ptr(v_out),
-                _ptr(reg),
-                _ptr(u0),
-                _stream_handle(stream),
-            )
-        )
+    def stage(self, scheme, stage, v_in, v_out, reg=None, u0=None, ghost_u=None, stream=None, lo=None, hi=None):
+        args = (self.handle, ctypes.byref(scheme), ctypes.byref(stage), _ptr(v_in), _ptr(ghost_u), _ptr(v_out),
+                _ptr(reg), _ptr(u0))
+        if lo is None and hi is None:
+            N.check(N.lib().fdg_rk_stage(*args, _stream_handle(stream)))
+        else:
+            N.check(N.lib().fdg_rk_stage_range(*args, int(0 if lo is None else lo),
+                                               int(self.n_elem if hi is None else hi), _stream_handle(stream)))
         return v_out
 
     def gate(self, u, stream=None):

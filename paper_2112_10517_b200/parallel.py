@@ -89,7 +89,9 @@ class HaloExchange:
 
     Works on CPU tensors with gloo (tests) and on CUDA tensors with NCCL;
     ``pack`` is the device packer (DeviceMesh.pack_faces) or None for the
-    host packer. Grouped send/recv to both ring neighbours.
+    host packer. Grouped send/recv to both ring neighbours. ``start`` /
+    ``finish`` split it so the interior elements run while it is in flight
+    (``split_launch``); calling the object does both (blocking).
     """
 
     def __init__(self, part, d, p1, torch, dist, device="cpu", pack=None, group=None):
@@ -108,9 +110,14 @@ class HaloExchange:
         self.first_idx = torch.as_tensor(part["send_first"], device=device)
         self.last_idx = torch.as_tensor(part["send_last"], device=device)
 
-    def __call__(self, u):
+    # ---- split API: start the exchange, run the interior, finish, run the boundary
+    def start(self, u):
+        """Pack this slab's two x-face planes of ``u`` and post the grouped
+        send/recv (asynchronous: NCCL queues it on its own stream behind the
+        packing kernels); ``finish`` waits for it and returns the ghosts."""
+        self._reqs = []
         if self.world == 1:
-            return None
+            return
         torch, dist = self.torch, self.dist
         if self.pack is not None:
             self.pack(u, self.first_idx, 0, 0, self.send_first)
@@ -121,16 +128,58 @@ class HaloExchange:
             self.send_last.copy_(torch.from_numpy(pack_faces_host(un, self.part["send_last"], self.d, self.p1, 0, 1)))
         F = self.part["plane"]
         nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
-        # tags disambiguate the two messages when both neighbours are one rank (W = 2)
+        # tags disambiguate the two messages when both neighbours are one rank
+        # (W = 2, gloo); NCCL matches them in posting order, which is the same
         ops = [
             dist.P2POp(dist.isend, self.send_first, prv, group=self.group, tag=1),
             dist.P2POp(dist.isend, self.send_last, nxt, group=self.group, tag=2),
             dist.P2POp(dist.irecv, self.ghost[:F], nxt, group=self.group, tag=1),
             dist.P2POp(dist.irecv, self.ghost[F:], prv, group=self.group, tag=2),
         ]
-        for req in dist.batch_isend_irecv(ops):
+        self._reqs = dist.batch_isend_irecv(ops)
+
+    def finish(self):
+        """Wait for the exchange posted by ``start`` (NCCL: the current CUDA
+        stream waits for it, the host does not) and return the ghost traces
+        (None on one rank)."""
+        for req in self._reqs:
             req.wait()
-        return self.ghost
+        self._reqs = []
+        return self.ghost if self.world > 1 else None
+
+    def __call__(self, u):
+        """Blocking exchange: ghosts of ``u`` for a whole-slab launch."""
+        self.start(u)
+        return self.finish()
+
+    def ranges(self, n_loc):
+        """(interior, boundary) element ranges of the split: the interior
+        elements read no ghost slot; the boundary ranges are the first and
+        last planes (merged when they touch)."""
+        F = self.part["plane"]
+        if self.world == 1:
+            return (0, n_loc), []
+        if n_loc <= 2 * F:
+            return None, [(0, n_loc)]
+        return (F, n_loc - F), [(0, F), (n_loc - F, n_loc)]
+
+
+def split_launch(halo, u, n_loc, launch):
+    """One RHS-type evaluation with the face-trace exchange overlapped:
+    ``launch(lo, hi, ghost)`` runs the kernel on elements [lo, hi). Order:
+    pack + post the exchange, the interior (no ghosts) while it is in flight,
+    wait, then the boundary planes with the received ghosts. Bitwise equal
+    to one whole-slab launch after a blocking exchange."""
+    if halo is None or halo.world == 1:
+        launch(None, None, None)
+        return
+    interior, boundary = halo.ranges(n_loc)
+    halo.start(u)
+    if interior is not None:
+        launch(interior[0], interior[1], None)
+    ghost = halo.finish()
+    for lo, hi in boundary:
+        launch(lo, hi, ghost)
 
 
 def combine_diagnostic(kind, local, dist, group=None):

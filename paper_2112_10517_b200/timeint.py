@@ -369,8 +369,22 @@ class DeviceStepper:
 
     def _launch(self, stages):
         for st, v_in, v_out, u0 in stages:
-            ghost = self.exchange(v_in) if self.exchange is not None else None
-            self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost)
+            self._stage(st, v_in, v_out, u0)
+
+    def _stage(self, st, v_in, v_out, u0):
+        """One fused stage; with a split-capable exchange (parallel.HaloExchange)
+        the interior elements run while the face traces are in flight."""
+        ex = self.exchange
+        if ex is not None and hasattr(ex, "start"):
+            from .parallel import split_launch
+
+            def launch(lo, hi, ghost):
+                self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost, lo=lo, hi=hi)
+
+            split_launch(ex, v_in, self.dm.n_elem, launch)
+            return
+        ghost = ex(v_in) if ex is not None else None
+        self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost)
 
     def step(self, u, dt, check=True, t=0.0):
         if not dt > 0.0:
@@ -390,8 +404,7 @@ class DeviceStepper:
         stages = self._stages(u, dt)
         for st, v_in, v_out, u0 in stages:
             self.dm.reset_status()
-            ghost = self.exchange(v_in) if self.exchange is not None else None
-            self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost)
+            self._stage(st, v_in, v_out, u0)
             first_bad, bad_stage = self.dm.read_status()
             if first_bad >= 0:
                 self.dm.raise_if_inadmissible(v_in, first_bad, self.dm.gamma)

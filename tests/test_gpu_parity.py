@@ -424,7 +424,8 @@ def test_device_stepper_graph_and_divergence():
 # --------------------------------------------------- partitioned device path
 
 
-@pytest.mark.parametrize("world,dims,p,amp", [(2, (4, 2, 3), 3, 0.0), (3, (6, 2, 2), 4, -0.1), (2, (4, 5), 3, 0.1)])
+@pytest.mark.parametrize("world,dims,p,amp", [(2, (4, 2, 3), 3, 0.0), (3, (6, 2, 2), 4, -0.1), (2, (4, 5), 3, 0.1),
+                                          (2, (8, 3, 5), 4, -0.1), (3, (9, 4, 3), 3, 0.0)])
 @pytest.mark.parametrize("kernel", ["reference", "batched"])
 def test_slab_partition_on_device_bitwise(world, dims, p, amp, kernel):
     """The ghost-slot path of the element kernel: W slabs on one GPU, face
@@ -464,6 +465,16 @@ def test_slab_partition_on_device_bitwise(world, dims, p, amp, kernel):
         ghost = torch.cat([first[(r + 1) % world], last[(r - 1) % world]])
         got = dm.rhs(ul, cfg.scheme(), ghost_u=ghost).cpu().numpy()
         assert np.array_equal(got, want[pt["lo"] : pt["hi"]]), r
+        # the overlap split: interior range WITHOUT ghosts, then the boundary planes
+        F, n = pt["plane"], pt["hi"] - pt["lo"]
+        out = torch.full_like(ul, float("nan"))
+        if n > 2 * F:
+            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=None, lo=F, hi=n - F)
+            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=0, hi=F)
+            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=n - F, hi=n)
+        else:
+            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=0, hi=n)
+        assert np.array_equal(out.cpu().numpy(), want[pt["lo"] : pt["hi"]]), ("split", r)
 
 
 # ---------------------------------------------------------------- diagnostics

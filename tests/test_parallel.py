@@ -63,6 +63,80 @@ def _worker(rank, world, port, dims, p, amp, vf, sf, results):
         dist.destroy_process_group()
 
 
+def _split_worker(rank, world, port, dims, p, amp, results):
+    """The overlap split (parallel.split_launch): interior rows computed
+    while the exchange is in flight with NO ghost buffer, boundary planes
+    after finish() with the ghosts -- bitwise the single-domain rows."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_2112_10517_b200 import GasParams, build_mesh, build_setup, lgl_operator, prim2cons
+    from paper_2112_10517_b200.parallel import HaloExchange, slab_partition, split_launch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gas = GasParams(1.4)
+        setup = build_setup(build_mesh(dims, bounds=(-1.0, 1.0), amplitude=amp), lgl_operator(p), gas)
+        rng = np.random.default_rng(12)
+        q = np.empty((setup.n_elements, setup.n_nodes, setup.d + 2))
+        q[..., 0] = 1.0 + 0.3 * rng.random(q.shape[:2])
+        q[..., 1 : setup.d + 1] = 0.3 * (rng.random(q.shape[:2] + (setup.d,)) - 0.5)
+        q[..., -1] = 1.0 + 0.3 * rng.random(q.shape[:2])
+        u = prim2cons(q, gas)
+        part = slab_partition(setup, rank, world)
+        lo, hi = part["lo"], part["hi"]
+        u_loc = np.ascontiguousarray(u[lo:hi])
+        halo = HaloExchange(part, setup.d, p + 1, torch, dist)
+        cart = setup.metrics.cartesian
+
+        def mesh(ghost):
+            return oracle.MeshArrays(
+                setup.d, p + 1, hi - lo, setup.dsplit.matrix, setup.op.weights, gas.gamma, gas.inv_gamma_minus_one,
+                cart, setup.metrics.areas if cart else None, setup.metrics.jac_const if cart else 0.0,
+                None if cart else setup.metrics.ja[lo:hi], None if cart else setup.metrics.jac[lo:hi],
+                part["plus"], part["minus"],
+                ghost_u=None if ghost is None else ghost.numpy(), ghost_nrm=part["ghost_nrm"],
+            )
+
+        du_loc = np.full_like(u_loc, np.nan)
+        calls = []
+
+        def launch(a, b, ghost):
+            a = 0 if a is None else a
+            b = hi - lo if b is None else b
+            calls.append((a, b, ghost is not None))
+            oracle.rhs_range(u_loc, mesh(ghost), du_loc, a, b, "ranocha", "llf")
+
+        split_launch(halo, torch.from_numpy(u_loc), hi - lo, launch)
+        du_all = oracle.rhs(u, setup, "ranocha", "llf")
+        interior_no_ghost = all(not g for a, b, g in calls if a > 0 and b < hi - lo)
+        results[rank] = (bool(np.array_equal(du_loc, du_all[lo:hi])), interior_no_ghost, len(calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,p,amp", [(2, (6, 2, 3), 3, 0.0), (3, (9, 2, 2), 4, -0.1), (2, (6, 3), 3, 0.1)])
+def test_overlap_split_bitwise(world, dims, p, amp):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    manager = ctx.Manager()
+    results = manager.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, dims, p, amp, results)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=180)
+        assert pr.exitcode == 0
+    for r in range(world):
+        ok, interior_no_ghost, n_calls = results[r]
+        assert ok and interior_no_ghost and n_calls == 3, (r, results[r])
+
+
 @pytest.mark.parametrize(
     "world,dims,p,amp",
     [(2, (4, 2, 3), 3, 0.0), (2, (2, 3, 2), 2, 0.08), (3, (6, 2, 2), 4, -0.1), (2, (4, 5), 3, 0.1)],
