@@ -587,7 +587,7 @@ def measure_sharded(kind, args, rank, world, local, dist):
     from paper_2112_10517_b200 import _native as N
     from paper_2112_10517_b200 import workloads
     from paper_2112_10517_b200.device import DeviceMesh
-    from paper_2112_10517_b200.parallel import HaloExchange, slab_partition, split_launch
+    from paper_2112_10517_b200.parallel import HALO_RESERVE_SMS, HaloExchange, slab_partition, split_launch
     from paper_2112_10517_b200.timeint import SSPRK43, DeviceStepper
 
     cfg = {"rhs4": 4, "rhs5": 5, "step4": 4}[kind]
@@ -599,6 +599,8 @@ def measure_sharded(kind, args, rank, world, local, dist):
     nodes_total = setup.n_elements * setup.n_nodes
     halo = HaloExchange(part, setup.d, setup.op.degree + 1, torch, dist, device="cuda", pack=dm.pack_faces) \
         if world > 1 else None
+    if halo is not None:
+        dm.reserve_sms(HALO_RESERVE_SMS)  # the exchange's kernels run beside the interior launch
     scheme = config.scheme()
     out = dm.empty()
     stepper = None

@@ -171,6 +171,14 @@ int fdg_read_status(fdg_mesh_t *mesh, fdg_status_t *out, void *stream);
  * array must outlive the mesh handle or the next call. */
 int fdg_mesh_set_traversal(fdg_mesh_t *mesh, const int32_t *row_order, int64_t row_len);
 
+/* interface launches (fdg_rhs*, fdg_rk_stage*, fdg_surface) size their
+ * persistent grid for sm_count - n_sms SMs: at full occupancy the element
+ * kernel holds every register of every SM, so a concurrent kernel (the halo
+ * packer, NCCL's send/recv) cannot start until it ends; the sharded RHS
+ * reserves a few SMs so the exchange overlaps the interior launch. Batches
+ * are claimed dynamically, so the smaller grid costs no load imbalance. */
+int fdg_mesh_set_reserve_sms(fdg_mesh_t *mesh, int32_t n_sms);
+
 /* diagnostics reductions over every node of the mesh (rank-local; sums and
  * the min combine across ranks with an all-reduce).  `a` = u, `b` = dudt
  * (ENTROPY) or u_exact (ERROR_SQ), else NULL; `out` is a DEVICE buffer of

@@ -105,6 +105,7 @@ EXPORTS = (
     "fdg_gate",
     "fdg_reset_status",
     "fdg_read_status",
+    "fdg_mesh_set_reserve_sms",
     "fdg_pack_faces",
     "fdg_fp64_probe",
 )
@@ -147,6 +148,7 @@ def lib():
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]
     L.fdg_mesh_set_traversal.argtypes = [vp, vp, ctypes.c_int64]
+    L.fdg_mesh_set_reserve_sms.argtypes = [vp, i32]
     L.fdg_build_geometry.argtypes = [P(GeometryDesc), vp, vp, vp, vp]
     L.fdg_diagnostic.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]

@@ -21,8 +21,11 @@ struct fdg_mesh {
     long long n_elem = 0;
     bool curved = false;
     int sm_count = 148;
+    int dyn_claim = 1;
+    int reserve_sms = 0;  // fdg_mesh_set_reserve_sms: interface launches leave these SMs' slots free
     KParams base{};
     Status* status = nullptr;       // device
+    unsigned long long* claim = nullptr;  // device: dynamic batch-claiming counter + done count (interface launches)
     Status* status_host = nullptr;  // page-locked read-back slot (a pageable D2H target is a slow, bounced copy)
     double w1d[8] = {};             // 1D LGL weights (diagnostics)
     double* diag_part = nullptr;    // (diag_blocks, kDiagQ) partials, allocated on first use
@@ -151,6 +154,25 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         return cuda_fail(err, "cudaMemset(status)");
     }
     k.status = m->status;
+    err = cudaMalloc(&m->claim, 2 * sizeof(unsigned long long));
+    if (err == cudaSuccess) err = cudaMemset(m->claim, 0, 2 * sizeof(unsigned long long));
+    if (err != cudaSuccess) {
+        cudaFree(m->status);
+        if (m->claim) cudaFree(m->claim);
+        delete m;
+        return cuda_fail(err, "cudaMalloc(claim counter)");
+    }
+    // interface epilogues (RHS, RK stage, surface) claim batches dynamically;
+    // the volume integral keeps the static order (FDG_DYN_CLAIM=0|1|2 tunes: off | interface | all)
+    {
+        const char* env = getenv("FDG_DYN_CLAIM");
+        m->dyn_claim = env ? atoi(env) : 1;
+        // runtime-direction volume pass in the p+1 <= 4 interface kernels:
+        // measured slower (cfg5 RHS 9.42 vs 8.92 ms with dynamic claiming,
+        // profiles/r02_ab_rt_dc.txt), off by default
+        const char* rt = getenv("FDG_RT_IFACE");
+        k.rt_iface = rt ? atoi(rt) : 0;
+    }
     {
         long long nn = 1;
         for (int i = 0; i < m->d; ++i) nn *= m->p1;
@@ -167,6 +189,7 @@ void fdg_mesh_destroy(fdg_mesh_t* m)
 {
     if (!m) return;
     if (m->status) cudaFree(m->status);
+    if (m->claim) cudaFree(m->claim);
     if (m->status_host) cudaFreeHost(m->status_host);
     if (m->diag_part) cudaFree(m->diag_part);
     if (m->s_in) cudaStreamDestroy(m->s_in);
@@ -217,6 +240,8 @@ static LaunchFn find(const fdg_mesh* m, const fdg_scheme_t* s, int vf)
 
 static int run(fdg_mesh* m, const fdg_scheme_t* s, KParams& k, int vf, void* stream)
 {
+    k.claim = (m->dyn_claim >= 2 || (m->dyn_claim == 1 && k.epilogue != EPI_VOLUME)) ? m->claim : nullptr;
+    k.reserve_sms = (k.epilogue != EPI_VOLUME) ? m->reserve_sms : 0;
     LaunchFn fn = find(m, s, vf);
     if (!fn) return fail(FDG_ERR_UNSUPPORTED, "no kernel for d=%d, p=%d, flux %s", m->d, m->p1 - 1, flux_name(vf));
     if (m->n_elem == 0) return FDG_OK;
@@ -475,6 +500,15 @@ int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "gate kernel launch");
     g_launches.fetch_add(1);
+    return FDG_OK;
+}
+
+int fdg_mesh_set_reserve_sms(fdg_mesh_t* m, int32_t n_sms)
+{
+    if (!m) return fail(FDG_ERR_ARG, "fdg_mesh_set_reserve_sms: null mesh");
+    if (n_sms < 0 || n_sms >= m->sm_count)
+        return fail(FDG_ERR_ARG, "fdg_mesh_set_reserve_sms: %d of %d SMs", n_sms, m->sm_count);
+    m->reserve_sms = n_sms;
     return FDG_OK;
 }
 

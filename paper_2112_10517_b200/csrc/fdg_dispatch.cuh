@@ -95,7 +95,7 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
     }
     const long long nb = (p.range_hi - p.range_lo + G::EPB - 1) / G::EPB;
     if (nb <= 0) return cudaSuccess;
-    const long long slots = (long long)bps * sm_count;
+    const long long slots = (long long)bps * std::max(1, sm_count - std::max(0, p.reserve_sms));
     if constexpr (twin) {
         if (nb > slots && nb <= (long long)bps_hi * sm_count) {
             return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>, (unsigned)nb, G::NT, smem, s, p);

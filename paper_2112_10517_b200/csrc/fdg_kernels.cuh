@@ -52,6 +52,10 @@ struct KParams {
     long long n_elem;         // elements of the mesh handle (neighbour-table stride)
     long long range_lo;       // this launch covers elements [range_lo, range_hi) (interior /
     long long range_hi;       //   boundary split of a partition); [0, n_elem) by default
+    unsigned long long* claim; // dynamic batch claiming: [0] next batch, [1] CTAs done (null: static grid-stride)
+    int rt_iface;             // interface epilogues below FDG_RT_DIR_MIN_P1 take the runtime-direction pass
+    int reserve_sms;          // launch only on sm_count - reserve_sms SMs' worth of CTAs (room for concurrent
+                              // halo kernels: a full-occupancy grid holds every register of every SM)
     long long elem_base;      // added to element indices reported by the gate
     double wts[3][64];        // per direction: Dsplit[a,b] * Ja^n_n (Cartesian) or Dsplit (curved)
     double areas[3];          // Cartesian Ja^n_n
@@ -379,6 +383,19 @@ __host__ __device__ constexpr bool runtime_direction()
 {
     return P1 >= FDG_RT_DIR_MIN_P1 && VF != F_CENTRAL;
 }
+// interface epilogues (RHS, RK stage) of the FAST kernels below that degree
+// also take the runtime-direction pass: the RHS kernel executes the volume
+// passes AND the face / stage code, and with three compile-time volume
+// passes its executed footprint overflowed the instruction cache (cfg5 RHS,
+// ncu r02: "no instruction" the largest stall reason, 22% of samples)
+#ifndef FDG_RT_DIR_IFACE
+#define FDG_RT_DIR_IFACE 1
+#endif
+template <int D, int P1, int VF>
+__host__ __device__ constexpr bool runtime_direction_iface()
+{
+    return FDG_RT_DIR_IFACE && VF != F_CENTRAL && !runtime_direction<D, P1, VF>();
+}
 
 template <int D, int P1, int VF, bool CURVED, int LOGS>
 __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const double* sq, double* sacc, int el, int m,
@@ -645,7 +662,34 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
     };
 
-    for (long long batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
+    // batch assignment: static grid-stride, or dynamic claiming in chunks of
+    // kClaim batches from a per-mesh counter (prm.claim) -- a CTA that becomes
+    // resident late (SMs held by concurrent work: the halo exchange's NCCL
+    // kernels next to an interior launch) then takes fewer batches instead of
+    // stretching the kernel's tail by its delay
+    constexpr long long kClaim = 4;
+    const bool dyn = prm.claim != nullptr;
+    __shared__ long long s_claim;
+    long long batch = blockIdx.x, chunk_end = 0;
+    if (dyn) {
+        if (tid == 0) s_claim = (long long)atomicAdd(prm.claim, (unsigned long long)kClaim);
+        __syncthreads();
+        batch = s_claim;
+        chunk_end = batch + kClaim;
+    }
+    auto advance = [&]() {
+        if (!dyn) {
+            batch += gridDim.x;
+            return;
+        }
+        if (++batch < chunk_end) return;
+        __syncthreads();
+        if (tid == 0) s_claim = (long long)atomicAdd(prm.claim, (unsigned long long)kClaim);
+        __syncthreads();
+        batch = s_claim;
+        chunk_end = batch + kClaim;
+    };
+    for (; batch < nbatch; advance()) {
         const long long e0 = first(batch);
         const int ne = (int)min((long long)EPB, prm.range_hi - e0);
         const long long base = e0 * NN * NVAR;
@@ -662,7 +706,8 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         // curved meshes) while this one computes: the next staging copy then
         // waits on L2, not HBM, latency
         {
-            const long long nb = batch + gridDim.x;
+            const long long nb = !dyn ? batch + gridDim.x
+                                 : (batch + 1 < chunk_end ? batch + 1 : batch + (long long)gridDim.x * kClaim);
             if (nb < nbatch) {
                 const long long f2 = first(nb);
                 const long long ne2 = min((long long)EPB, prm.range_hi - f2);
@@ -791,13 +836,17 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             __syncthreads();
             FDG_PT(1)
             // ---- volume integral, direction by direction (accumulators: SoA)
-            if constexpr (MODE == FAST && runtime_direction<D, P1, VF>()) {
+            bool rt_pass = MODE == FAST && runtime_direction<D, P1, VF>();
+            if constexpr (MODE == FAST && runtime_direction_iface<D, P1, VF>()) rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;
+            if (rt_pass) {
+                if constexpr (MODE == FAST && VF != F_CENTRAL) {
 #pragma unroll 1
-                for (int n = 0; n < D; ++n) {
-                    if (vmask) volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, vmask);
-                    __syncthreads();
+                    for (int n = 0; n < D; ++n) {
+                        if (vmask) volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, vmask);
+                        __syncthreads();
+                    }
                 }
-            } else {
+            } else if constexpr (!(MODE == FAST && runtime_direction<D, P1, VF>())) {
                 vdir<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e, active, vmask);
                 __syncthreads();
                 FDG_PT(2)
@@ -948,6 +997,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         tma_pending = tma_out;
     }
     if (tma_out_ok && tid == 0) bulk_wait_all();
+    if (dyn && tid == 0) {
+        // the last CTA out resets the counter for the next launch on this mesh
+        // (every CTA has left its loop, so nothing claims after the reset)
+        __threadfence();
+        if (atomicAdd(prm.claim + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+            atomicExch(prm.claim, 0ull);
+            atomicExch(prm.claim + 1, 0ull);
+        }
+    }
 #if FDG_PHASE_TIMING
     if (tid == 0)
         for (int i = 0; i < 8; ++i) atomicAdd(&fdg_phase_cycles[i], (unsigned long long)pt_[i]);

@@ -168,6 +168,12 @@ class DeviceMesh:
         self.row_order = self.torch.as_tensor(r.astype(np.int32), device=self.device)
         N.check(N.lib().fdg_mesh_set_traversal(self.handle, _ptr(self.row_order), n2))
 
+    def reserve_sms(self, n):
+        """Leave ``n`` SMs' worth of CTA slots free in interface launches
+        (fdg_mesh_set_reserve_sms): room for the halo kernels to run
+        concurrently with the interior elements."""
+        N.check(N.lib().fdg_mesh_set_reserve_sms(self.handle, int(n)))
+
     # ------------------------------------------------------------ shapes
     @property
     def shape(self):

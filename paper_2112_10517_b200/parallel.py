@@ -164,6 +164,9 @@ class HaloExchange:
         return (F, n_loc - F), [(0, F), (n_loc - F, n_loc)]
 
 
+HALO_RESERVE_SMS = 4  # SMs left to the packer / NCCL while the interior runs (DeviceMesh.reserve_sms)
+
+
 def split_launch(halo, u, n_loc, launch):
     """One RHS-type evaluation with the face-trace exchange overlapped:
     ``launch(lo, hi, ghost)`` runs the kernel on elements [lo, hi). Order:

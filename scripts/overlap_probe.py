@@ -40,10 +40,12 @@ def main():
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--comm-us", type=float, default=40.0)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--reserve", type=int, default=4, help="SMs left free in interface launches")
     a = ap.parse_args()
     setup, u_full, config = workloads.build_device(a.cfg, kernel="batched")
     part = slab_partition(setup, a.rank, a.world)
     dm = DeviceMesh(setup, partition=part)
+    dm.reserve_sms(a.reserve)
     lo, hi = part["lo"], part["hi"]
     u = u_full[lo:hi].clone()
     F, n = part["plane"], hi - lo
@@ -58,7 +60,8 @@ def main():
     scheme = config.scheme()
     out = dm.empty()
     ref = dm.empty()
-    main_s = torch.cuda.current_stream()
+    main_s = torch.cuda.Stream() if os.environ.get("PROBE_MAIN_STREAM", "own") == "own" else torch.cuda.current_stream()
+    torch.cuda.set_stream(main_s)
     side = torch.cuda.Stream()
     clock = torch.cuda.get_device_properties(0).clock_rate if hasattr(torch.cuda.get_device_properties(0), "clock_rate") else 1965000
     cycles = int(a.comm_us * 1e-6 * clock * 1e3)
@@ -113,12 +116,15 @@ def main():
     def exchange_only():
         exchange(main_s)
 
-    res = {"cfg": a.cfg, "world": a.world, "rank": a.rank, "slab_elements": n, "plane": F,
+    def interior_only():
+        dm.rhs(u, scheme, out=out, lo=F, hi=n - F)
+
+    res = {"cfg": a.cfg, "world": a.world, "rank": a.rank, "slab_elements": n, "plane": F, "reserve_sms": a.reserve,
            "comm_emulated_us": a.comm_us}
-    for name, f in (("exchange_only", exchange_only), ("whole", whole), ("split", split), ("serial", serial),
-                    ("overlapped", overlapped)):
+    for name, f in (("exchange_only", exchange_only), ("interior_only", interior_only), ("whole", whole),
+                    ("split", split), ("serial", serial), ("overlapped", overlapped)):
         res[name + "_ms"] = timed(f)
-        if name != "exchange_only":
+        if name not in ("exchange_only", "interior_only"):
             res[name + "_bitwise"] = bool(torch.equal(out, ref))
     res["hidden_fraction"] = (res["serial_ms"] - res["overlapped_ms"]) / max(res["exchange_only_ms"], 1e-9)
     print(json.dumps(res))
