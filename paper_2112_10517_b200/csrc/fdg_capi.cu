@@ -630,8 +630,19 @@ int fdg_pack_faces(const double* u, const int32_t* elems, int32_t n, int32_t d, 
     if ((d != 2 && d != 3) || degree < 1 || dir < 0 || dir >= d) return fail(FDG_ERR_ARG, "fdg_pack_faces: bad shape");
     if (n == 0) return FDG_OK;
     const int threads = 256;
-    const int blocks = 296;
-    pack_faces_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(u, elems, n, d, degree + 1, dir, side, out);
+    if (dir == 0) {
+        const long long p1 = degree + 1, nvar = d + 2;
+        long long fn = 1;
+        for (int i = 0; i < d - 1; ++i) fn *= p1;
+        const long long run = fn * nvar, elem = fn * p1 * nvar;
+        const long long off = side ? (p1 - 1) * run : 0;
+        const long long work = (long long)n * run / 2;
+        const int blocks = (int)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, 148LL * 8));
+        pack_faces_dir0_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(u, elems, n, elem, run, off, out);
+    } else {
+        const int blocks = 296;
+        pack_faces_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(u, elems, n, d, degree + 1, dir, side, out);
+    }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "pack kernel launch");
     g_launches.fetch_add(1);

@@ -59,7 +59,14 @@ def slab_partition(setup, rank, world):
         ends = node_lines(p1, d)[0][:, -1]  # +x face nodes, line order
         remote_minus = minus_g[0, lo : lo + F]  # previous rank's last plane
         ghost_nrm = np.zeros((2 * F, fn, d))
-        ghost_nrm[F:] = np.asarray(setup.metrics.ja)[remote_minus][:, ends, 0, :]
+        ja = setup.metrics.ja
+        if hasattr(ja, "is_cuda"):  # device-built geometry: gather on the device, copy the small result
+            import torch
+
+            sel = ja[torch.as_tensor(remote_minus, device=ja.device)][:, torch.as_tensor(ends, device=ja.device), 0, :]
+            ghost_nrm[F:] = sel.cpu().numpy()
+        else:
+            ghost_nrm[F:] = np.asarray(ja)[remote_minus][:, ends, 0, :]
     return {
         "rank": rank,
         "world": world,
@@ -164,7 +171,7 @@ class HaloExchange:
         return (F, n_loc - F), [(0, F), (n_loc - F, n_loc)]
 
 
-HALO_RESERVE_SMS = 4  # SMs left to the packer / NCCL while the interior runs (DeviceMesh.reserve_sms)
+HALO_RESERVE_SMS = 8  # SMs left to the packer / NCCL while the interior runs (DeviceMesh.reserve_sms)
 
 
 def split_launch(halo, u, n_loc, launch):

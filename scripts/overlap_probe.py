@@ -40,7 +40,7 @@ def main():
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--comm-us", type=float, default=40.0)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--reserve", type=int, default=4, help="SMs left free in interface launches")
+    ap.add_argument("--reserve", type=int, default=8, help="SMs left free in interface launches")
     a = ap.parse_args()
     setup, u_full, config = workloads.build_device(a.cfg, kernel="batched")
     part = slab_partition(setup, a.rank, a.world)
@@ -102,10 +102,16 @@ def main():
         whole()
 
     def overlapped():
+        # the real order (parallel.split_launch): pack on the compute stream,
+        # the wire (NCCL) on its own stream beside the interior launch
+        dm.pack_faces(u_full, nxt_first, 0, 0, stage[:F], stream=main_s)
+        dm.pack_faces(u_full, prv_last, 0, 1, stage[F:], stream=main_s)
         ev = torch.cuda.Event()
         ev.record(main_s)
         side.wait_event(ev)
-        exchange(side)
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(cycles)  # the wire
+            ghost.copy_(stage)
         dm.rhs(u, scheme, out=out, lo=F, hi=n - F)
         done = torch.cuda.Event()
         done.record(side)
