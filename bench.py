@@ -608,14 +608,14 @@ def measure_sharded(kind, args, rank, world, local, dist):
         stepper = DeviceStepper(dm, config, SSPRK43, exchange=halo)
         dt = 1e-4
 
-    def launch(lo, hi, ghost):
-        dm.rhs(u, scheme, out=out, ghost_u=ghost, lo=lo, hi=hi)
+    def launch(ranges, ghost):
+        dm.rhs(u, scheme, out=out, ghost_u=ghost, ranges=ranges)
 
     def step(i):
         if stepper is not None:
             return stepper.step(u, dt, check=False)
         # interior elements while the face traces are in flight, then the two boundary planes
-        split_launch(halo, u, dm.n_elem, launch)
+        split_launch(halo, u, dm.n_elem, launch, dm.nn)
 
     for i in range(args.warmup):
         step(i)

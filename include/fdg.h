@@ -144,18 +144,19 @@ int fdg_rhs(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, const
 /* one Runge-Kutta stage fused with the RHS: v_out must not alias v_in */
 int fdg_rk_stage(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const fdg_stage_t *stage, const double *v_in,
                  const double *ghost_u, double *v_out, double *reg, const double *u0, void *stream);
-/* fdg_rhs / fdg_rk_stage restricted to the local elements [elem_lo, elem_hi)
- * (u, du, v_in, v_out, reg, u0: the whole arrays; only the range's rows are
+/* fdg_rhs / fdg_rk_stage restricted to the local elements [lo, hi) plus an
+ * optional second range [lo2, hi2) (empty: lo2 == hi2) in the same launch
+ * (u, du, v_in, v_out, reg, u0: the whole arrays; only those rows are
  * written). The overlap split of a slab partition: the interior elements
  * never read ghost_u (NULL is fine) and run while the face-trace exchange is
- * in flight; the boundary planes run after it with the received ghosts.
- * Results are bitwise those of the whole-slab call (every element's
- * arithmetic is independent of which launch covers it). */
+ * in flight; the two boundary planes run after it, in one launch, with the
+ * received ghosts. Results are bitwise those of the whole-slab call (every
+ * element's arithmetic is independent of which launch covers it). */
 int fdg_rhs_range(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const double *u, const double *ghost_u, double *du,
-                  int64_t elem_lo, int64_t elem_hi, void *stream);
+                  int64_t lo, int64_t hi, int64_t lo2, int64_t hi2, void *stream);
 int fdg_rk_stage_range(fdg_mesh_t *mesh, const fdg_scheme_t *scheme, const fdg_stage_t *stage, const double *v_in,
-                       const double *ghost_u, double *v_out, double *reg, const double *u0, int64_t elem_lo,
-                       int64_t elem_hi, void *stream);
+                       const double *ghost_u, double *v_out, double *reg, const double *u0, int64_t lo, int64_t hi,
+                       int64_t lo2, int64_t hi2, void *stream);
 /* admissibility of every node (rho > 0, p > 0, finite) into the status record */
 int fdg_gate(fdg_mesh_t *mesh, const double *u, void *stream);
 int fdg_reset_status(fdg_mesh_t *mesh, void *stream);

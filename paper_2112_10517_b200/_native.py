@@ -142,8 +142,9 @@ def lib():
     L.fdg_surface.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rhs.argtypes = [vp, P(Scheme), vp, vp, vp, vp]
     L.fdg_rk_stage.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, vp]
-    L.fdg_rhs_range.argtypes = [vp, P(Scheme), vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
-    L.fdg_rk_stage_range.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
+    i64 = ctypes.c_int64
+    L.fdg_rhs_range.argtypes = [vp, P(Scheme), vp, vp, vp, i64, i64, i64, i64, vp]
+    L.fdg_rk_stage_range.argtypes = [vp, P(Scheme), P(Stage), vp, vp, vp, vp, vp, i64, i64, i64, i64, vp]
     L.fdg_gate.argtypes = [vp, vp, vp]
     L.fdg_reset_status.argtypes = [vp, vp]
     L.fdg_read_status.argtypes = [vp, P(StatusRec), vp]

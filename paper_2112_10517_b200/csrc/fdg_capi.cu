@@ -414,15 +414,25 @@ static int check_range(const fdg_mesh* m, int64_t lo, int64_t hi, const char* wh
     return FDG_OK;
 }
 
+static int check_ranges(const fdg_mesh* m, int64_t lo, int64_t hi, int64_t lo2, int64_t hi2, const char* who)
+{
+    int rc = check_range(m, lo, hi, who);
+    if (!rc) rc = check_range(m, lo2, hi2, who);
+    if (!rc && lo2 < hi2 && lo < hi && lo2 < hi && lo < hi2)
+        return fail(FDG_ERR_ARG, "%s: ranges [%lld, %lld) and [%lld, %lld) overlap", who, (long long)lo, (long long)hi,
+                    (long long)lo2, (long long)hi2);
+    return rc;
+}
+
 int fdg_rhs_range(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double* ghost_u, double* du, int64_t lo,
-                  int64_t hi, void* stream)
+                  int64_t hi, int64_t lo2, int64_t hi2, void* stream)
 {
     if (!m || !u || !du) return fail(FDG_ERR_ARG, "fdg_rhs: null argument");
     if (u == du) return fail(FDG_ERR_ARG, "fdg_rhs: du must not alias u");
     int rc = check_scheme(s, true, true);
-    if (!rc) rc = check_range(m, lo, hi, "fdg_rhs_range");
+    if (!rc) rc = check_ranges(m, lo, hi, lo2, hi2, "fdg_rhs_range");
     if (rc) return rc;
-    if (lo == hi) return FDG_OK;
+    if (lo == hi && lo2 == hi2) return FDG_OK;
     KParams k = m->base;
     k.u = u;
     k.out = du;
@@ -432,6 +442,8 @@ int fdg_rhs_range(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const d
     k.precompute = s->precompute;
     k.range_lo = lo;
     k.range_hi = hi;
+    k.range2_lo = lo2;
+    k.range2_hi = hi2;
     return run(m, s, k, s->volume_flux, stream);
 }
 
@@ -439,12 +451,12 @@ int fdg_rhs(fdg_mesh_t* m, const fdg_scheme_t* s, const double* u, const double*
             void* stream)
 {
     if (!m) return fail(FDG_ERR_ARG, "fdg_rhs: null argument");
-    return fdg_rhs_range(m, s, u, ghost_u, du, 0, m->n_elem, stream);
+    return fdg_rhs_range(m, s, u, ghost_u, du, 0, m->n_elem, 0, 0, stream);
 }
 
 int fdg_rk_stage_range(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, const double* v_in,
                        const double* ghost_u, double* v_out, double* reg, const double* u0, int64_t lo, int64_t hi,
-                       void* stream)
+                       int64_t lo2, int64_t hi2, void* stream)
 {
     if (!m || !st || !v_in || !v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: null argument");
     if (v_in == v_out) return fail(FDG_ERR_ARG, "fdg_rk_stage: v_out must not alias v_in");
@@ -452,9 +464,9 @@ int fdg_rk_stage_range(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* 
     if (st->kind == 1 && st->a != 0.0 && !u0) return fail(FDG_ERR_ARG, "fdg_rk_stage: stage needs u0");
     if (st->kind != 0 && st->kind != 1) return fail(FDG_ERR_CONFIG, "stage kind %d unknown", st->kind);
     int rc = check_scheme(s, true, true);
-    if (!rc) rc = check_range(m, lo, hi, "fdg_rk_stage_range");
+    if (!rc) rc = check_ranges(m, lo, hi, lo2, hi2, "fdg_rk_stage_range");
     if (rc) return rc;
-    if (lo == hi) return FDG_OK;
+    if (lo == hi && lo2 == hi2) return FDG_OK;
     KParams k = m->base;
     k.u = v_in;
     k.out = v_out;
@@ -472,6 +484,8 @@ int fdg_rk_stage_range(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* 
     k.dt = st->dt;
     k.range_lo = lo;
     k.range_hi = hi;
+    k.range2_lo = lo2;
+    k.range2_hi = hi2;
     return run(m, s, k, s->volume_flux, stream);
 }
 
@@ -479,7 +493,7 @@ int fdg_rk_stage(fdg_mesh_t* m, const fdg_scheme_t* s, const fdg_stage_t* st, co
                  const double* ghost_u, double* v_out, double* reg, const double* u0, void* stream)
 {
     if (!m) return fail(FDG_ERR_ARG, "fdg_rk_stage: null argument");
-    return fdg_rk_stage_range(m, s, st, v_in, ghost_u, v_out, reg, u0, 0, m->n_elem, stream);
+    return fdg_rk_stage_range(m, s, st, v_in, ghost_u, v_out, reg, u0, 0, m->n_elem, 0, 0, stream);
 }
 
 int fdg_gate(fdg_mesh_t* m, const double* u, void* stream)

@@ -93,7 +93,7 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
             bps_tab[dev] = bps;  // published last: a reader seeing bps > 0 sees bps_hi
         }
     }
-    const long long nb = (p.range_hi - p.range_lo + G::EPB - 1) / G::EPB;
+    const long long nb = (p.range_hi - p.range_lo + G::EPB - 1) / G::EPB + (p.range2_hi - p.range2_lo + G::EPB - 1) / G::EPB;
     if (nb <= 0) return cudaSuccess;
     const long long slots = (long long)bps * std::max(1, sm_count - std::max(0, p.reserve_sms));
     if constexpr (twin) {

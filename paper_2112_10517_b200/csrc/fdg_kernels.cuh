@@ -52,6 +52,8 @@ struct KParams {
     long long n_elem;         // elements of the mesh handle (neighbour-table stride)
     long long range_lo;       // this launch covers elements [range_lo, range_hi) (interior /
     long long range_hi;       //   boundary split of a partition); [0, n_elem) by default
+    long long range2_lo;      // optional second range [range2_lo, range2_hi) in the same launch
+    long long range2_hi;      //   (both boundary planes of a slab in one launch); empty by default
     unsigned long long* claim; // dynamic batch claiming: [0] next batch, [1] CTAs done (null: static grid-stride)
     int rt_iface;             // interface epilogues below FDG_RT_DIR_MIN_P1 take the runtime-direction pass
     int reserve_sms;          // launch only on sm_count - reserve_sms SMs' worth of CTAs (room for concurrent
@@ -643,7 +645,9 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     // warps -- a compile-time full mask when the CTA has no spare threads
     constexpr int USED = EPB * G::LINES;
     const unsigned vmask = (USED == NT) ? 0xffffffffu : __ballot_sync(0xffffffffu, tid < USED) * (tid < USED);
-    const long long nbatch = (prm.range_hi - prm.range_lo + EPB - 1) / EPB;
+    const long long nb1 = (prm.range_hi - prm.range_lo + EPB - 1) / EPB;
+    const long long nbatch = nb1 + (prm.range2_hi - prm.range2_lo + EPB - 1) / EPB;
+    auto range_end = [&](long long b) -> long long { return b < nb1 ? prm.range_hi : prm.range2_hi; };
     const int epi = prm.epilogue;
 #if FDG_NB_SMEM
     __shared__ int s_nb[EPB * 2 * D];
@@ -656,7 +660,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     // hits) instead of 16384 elements away; batches never straddle rows.
     const bool remap = prm.row_order && (prm.row_len % EPB) == 0 && prm.range_lo == 0 && prm.range_hi == prm.n_elem;
     auto first = [&](long long b) -> long long {
-        const long long f = prm.range_lo + b * EPB;
+        const long long f = b < nb1 ? prm.range_lo + b * EPB : prm.range2_lo + (b - nb1) * EPB;
         if (!remap) return f;
         const long long r = f / prm.row_len;
         return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     };
     for (; batch < nbatch; advance()) {
         const long long e0 = first(batch);
-        const int ne = (int)min((long long)EPB, prm.range_hi - e0);
+        const int ne = (int)min((long long)EPB, range_end(batch) - e0);
         const long long base = e0 * NN * NVAR;
         const int count = ne * NN * NVAR;
         const long long e = e0 + el;
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                                  : (batch + 1 < chunk_end ? batch + 1 : batch + (long long)gridDim.x * kClaim);
             if (nb < nbatch) {
                 const long long f2 = first(nb);
-                const long long ne2 = min((long long)EPB, prm.range_hi - f2);
+                const long long ne2 = min((long long)EPB, range_end(nb) - f2);
                 const char* p0 = reinterpret_cast<const char*>(prm.u + f2 * NN * NVAR);
                 const int bytes = (int)(ne2 * NN * NVAR * 8);
                 for (int off = tid * 128; off < bytes; off += NT * 128)

@@ -246,27 +246,40 @@ class DeviceMesh:
         )
         return out
 
-    def rhs(self, u, scheme, out=None, ghost_u=None, stream=None, lo=None, hi=None):
-        """du = -(VOL + SURF); with ``lo``/``hi`` only the local elements
-        [lo, hi) (fdg_rhs_range: the overlap split of a slab)."""
-        out = self.empty() if out is None else out
+    def _ranges(self, lo, hi, ranges):
+        """(lo, hi, lo2, hi2) of a range launch, or None for the whole mesh."""
+        if ranges is not None:
+            rs = list(ranges)
+            if not 1 <= len(rs) <= 2:
+                raise ValueError("one or two element ranges, got %d" % len(rs))
+            (a, b), (c, d) = rs[0], (rs[1] if len(rs) == 2 else (0, 0))
+            return int(a), int(b), int(c), int(d)
         if lo is None and hi is None:
+            return None
+        return int(0 if lo is None else lo), int(self.n_elem if hi is None else hi), 0, 0
+
+    def rhs(self, u, scheme, out=None, ghost_u=None, stream=None, lo=None, hi=None, ranges=None):
+        """du = -(VOL + SURF); with ``lo``/``hi`` (or up to two ``ranges``)
+        only those local elements (fdg_rhs_range: the overlap split)."""
+        out = self.empty() if out is None else out
+        r = self._ranges(lo, hi, ranges)
+        if r is None:
             N.check(N.lib().fdg_rhs(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out),
                                     _stream_handle(stream)))
         else:
-            N.check(N.lib().fdg_rhs_range(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out),
-                                          int(0 if lo is None else lo), int(self.n_elem if hi is None else hi),
+            N.check(N.lib().fdg_rhs_range(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(ghost_u), _ptr(out), *r,
                                           _stream_handle(stream)))
         return out
 
-    def stage(self, scheme, stage, v_in, v_out, reg=None, u0=None, ghost_u=None, stream=None, lo=None, hi=None):
+    def stage(self, scheme, stage, v_in, v_out, reg=None, u0=None, ghost_u=None, stream=None, lo=None, hi=None,
+              ranges=None):
         args = (self.handle, ctypes.byref(scheme), ctypes.byref(stage), _ptr(v_in), _ptr(ghost_u), _ptr(v_out),
                 _ptr(reg), _ptr(u0))
-        if lo is None and hi is None:
+        r = self._ranges(lo, hi, ranges)
+        if r is None:
             N.check(N.lib().fdg_rk_stage(*args, _stream_handle(stream)))
         else:
-            N.check(N.lib().fdg_rk_stage_range(*args, int(0 if lo is None else lo),
-                                               int(self.n_elem if hi is None else hi), _stream_handle(stream)))
+            N.check(N.lib().fdg_rk_stage_range(*args, *r, _stream_handle(stream)))
         return v_out
 
     def gate(self, u, stream=None):

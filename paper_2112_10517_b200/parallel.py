@@ -161,8 +161,8 @@ class HaloExchange:
 
     def ranges(self, n_loc):
         """(interior, boundary) element ranges of the split: the interior
-        elements read no ghost slot; the boundary ranges are the first and
-        last planes (merged when they touch)."""
+        elements read no ghost slot; the boundary is the first and last
+        planes (one range when they touch), run as ONE launch."""
         F = self.part["plane"]
         if self.world == 1:
             return (0, n_loc), []
@@ -172,24 +172,35 @@ class HaloExchange:
 
 
 HALO_RESERVE_SMS = 8  # SMs left to the packer / NCCL while the interior runs (DeviceMesh.reserve_sms)
+# the split pays one extra launch (its ramp and tail, ~20-90 us measured on
+# B200, profiles/r02_overlap_c.jsonl) to hide the exchange; below this many
+# planes per slab, or this many nodes, the blocking exchange + one launch wins
+SPLIT_MIN_PLANES = 8
+SPLIT_MIN_NODES = 1 << 22
 
 
-def split_launch(halo, u, n_loc, launch):
+def split_launch(halo, u, n_loc, launch, nodes_per_elem=None):
     """One RHS-type evaluation with the face-trace exchange overlapped:
-    ``launch(lo, hi, ghost)`` runs the kernel on elements [lo, hi). Order:
-    pack + post the exchange, the interior (no ghosts) while it is in flight,
-    wait, then the boundary planes with the received ghosts. Bitwise equal
-    to one whole-slab launch after a blocking exchange."""
+    ``launch(ranges, ghost)`` runs the kernel on the element ``ranges``
+    (None: the whole slab). Order: pack + post the exchange, the interior (no
+    ghosts) while it is in flight, wait, then both boundary planes in one
+    launch with the received ghosts. Bitwise equal to one whole-slab launch
+    after a blocking exchange. Small slabs (fewer than SPLIT_MIN_PLANES
+    planes or SPLIT_MIN_NODES nodes) take that blocking path."""
     if halo is None or halo.world == 1:
-        launch(None, None, None)
+        launch(None, None)
+        return
+    F = halo.part["plane"]
+    big = n_loc >= SPLIT_MIN_PLANES * F and (nodes_per_elem is None or n_loc * nodes_per_elem >= SPLIT_MIN_NODES)
+    if not big:
+        launch(None, halo(u))
         return
     interior, boundary = halo.ranges(n_loc)
     halo.start(u)
     if interior is not None:
-        launch(interior[0], interior[1], None)
+        launch([interior], None)
     ghost = halo.finish()
-    for lo, hi in boundary:
-        launch(lo, hi, ghost)
+    launch(boundary, ghost)
 
 
 def combine_diagnostic(kind, local, dist, group=None):

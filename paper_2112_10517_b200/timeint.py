@@ -378,10 +378,10 @@ class DeviceStepper:
         if ex is not None and hasattr(ex, "start"):
             from .parallel import split_launch
 
-            def launch(lo, hi, ghost):
-                self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost, lo=lo, hi=hi)
+            def launch(ranges, ghost):
+                self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost, ranges=ranges)
 
-            split_launch(ex, v_in, self.dm.n_elem, launch)
+            split_launch(ex, v_in, self.dm.n_elem, launch, self.dm.nn)
             return
         ghost = ex(v_in) if ex is not None else None
         self.dm.stage(self.scheme, st, v_in, v_out, reg=self.reg, u0=u0, ghost_u=ghost)

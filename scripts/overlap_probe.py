@@ -94,8 +94,7 @@ def main():
 
     def split():
         dm.rhs(u, scheme, out=out, lo=F, hi=n - F)
-        dm.rhs(u, scheme, out=out, ghost_u=ghost, lo=0, hi=F)
-        dm.rhs(u, scheme, out=out, ghost_u=ghost, lo=n - F, hi=n)
+        dm.rhs(u, scheme, out=out, ghost_u=ghost, ranges=[(0, F), (n - F, n)])
 
     def serial():
         exchange(main_s)
@@ -116,8 +115,7 @@ def main():
         done = torch.cuda.Event()
         done.record(side)
         main_s.wait_event(done)
-        dm.rhs(u, scheme, out=out, ghost_u=ghost, lo=0, hi=F)
-        dm.rhs(u, scheme, out=out, ghost_u=ghost, lo=n - F, hi=n)
+        dm.rhs(u, scheme, out=out, ghost_u=ghost, ranges=[(0, F), (n - F, n)])
 
     def exchange_only():
         exchange(main_s)

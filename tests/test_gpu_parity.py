@@ -470,8 +470,7 @@ def test_slab_partition_on_device_bitwise(world, dims, p, amp, kernel):
         out = torch.full_like(ul, float("nan"))
         if n > 2 * F:
             dm.rhs(ul, cfg.scheme(), out=out, ghost_u=None, lo=F, hi=n - F)
-            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=0, hi=F)
-            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=n - F, hi=n)
+            dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, ranges=[(0, F), (n - F, n)])
         else:
             dm.rhs(ul, cfg.scheme(), out=out, ghost_u=ghost, lo=0, hi=n)
         assert np.array_equal(out.cpu().numpy(), want[pt["lo"] : pt["hi"]]), ("split", r)

@@ -72,8 +72,10 @@ def _split_worker(rank, world, port, dims, p, amp, results):
 
     from oracle import oracle
     from paper_2112_10517_b200 import GasParams, build_mesh, build_setup, lgl_operator, prim2cons
+    from paper_2112_10517_b200 import parallel as PL
     from paper_2112_10517_b200.parallel import HaloExchange, slab_partition, split_launch
 
+    PL.SPLIT_MIN_PLANES = 3  # these tiny slabs take the split path
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -104,11 +106,10 @@ def _split_worker(rank, world, port, dims, p, amp, results):
         du_loc = np.full_like(u_loc, np.nan)
         calls = []
 
-        def launch(a, b, ghost):
-            a = 0 if a is None else a
-            b = hi - lo if b is None else b
-            calls.append((a, b, ghost is not None))
-            oracle.rhs_range(u_loc, mesh(ghost), du_loc, a, b, "ranocha", "llf")
+        def launch(ranges, ghost):
+            for a, b in (ranges if ranges is not None else [(0, hi - lo)]):
+                calls.append((a, b, ghost is not None))
+                oracle.rhs_range(u_loc, mesh(ghost), du_loc, a, b, "ranocha", "llf")
 
         split_launch(halo, torch.from_numpy(u_loc), hi - lo, launch)
         du_all = oracle.rhs(u, setup, "ranocha", "llf")
