@@ -208,6 +208,47 @@ typedef struct fdg_geometry_desc {
 } fdg_geometry_desc_t;
 int fdg_build_geometry(const fdg_geometry_desc_t *desc, double *coords, double *ja, double *jac, void *stream);
 
+/* ---- Gauss-node family (the paper's second scheme family):
+ * volume_scheme "gauss_fluxdiff" / "gauss_surface_correction" of the
+ * reference's rhs (discretization.py:966-995), i.e. the zero-corner
+ * hybridized flux-differencing volume term with entropy-projected face
+ * states (_project_all, :811-837) plus the interface fluxes of the projected
+ * states lifted through the dense boundary rows (_gauss_surface, :839-895).
+ * The two schemes differ only in the volume pair weights the host passes
+ * (hybridized Q_h entries vs the split-derivative matrix, operators.py:300-357). */
+typedef struct fdg_gauss fdg_gauss_t;
+typedef struct fdg_gauss_desc {
+    int32_t d;             /* 2 (p <= 7) or 3 (p <= 5) */
+    int32_t degree;
+    int64_t n_elem;
+    double gamma, inv_gamma_minus_one;
+    const double *boundary_interp; /* HOST (2, p+1): R rows at -1 / +1 */
+    const double *vv;      /* HOST (p+1, p+1): volume pair weights c_ab, a != b */
+    const double *cvol;    /* HOST (2, p+1): crossing weight into the volume row */
+    const double *cface;   /* HOST (2, p+1): crossing weight into the face row */
+    const double *lift;    /* HOST (2, p+1): R[s][a] / w[a] */
+    const double *ja;      /* DEVICE (n_elem, nn, d, d) metric terms at the Gauss nodes */
+    const double *jac;     /* DEVICE (n_elem, nn) */
+    const int32_t *plus;   /* DEVICE (d, n_elem) periodic neighbours */
+    const int32_t *minus;  /* DEVICE (d, n_elem) */
+} fdg_gauss_desc_t;
+int fdg_gauss_create(const fdg_gauss_desc_t *desc, fdg_gauss_t **out);
+void fdg_gauss_destroy(fdg_gauss_t *g);
+/* entropy-projected face states proj (n_elem, d, 2, fn, d+2) and each
+ * element's own face metric traces nrm (n_elem, d, 2, fn, d); NULL outputs go
+ * to library-owned scratch (allocated at creation) */
+int fdg_gauss_project(fdg_gauss_t *g, const double *u, double *proj, double *nrm, void *stream);
+/* du = -(VOL + SURF) / J of the Gauss schemes; proj/nrm NULL: projected first
+ * (fdg_gauss_project into the scratch); fnrm (n_elem, d, fn, d) interface
+ * normals or NULL (the minus element's side-1 traces) */
+int fdg_gauss_rhs(fdg_gauss_t *g, const fdg_scheme_t *scheme, const double *u, const double *proj, const double *nrm,
+                  const double *fnrm, double *du, void *stream);
+/* status: first_bad = first inadmissible node (gate), bad_stage = first
+ * direction*2+side whose projected state is inadmissible (entropy2cons) */
+int fdg_gauss_gate(fdg_gauss_t *g, const double *u, void *stream);
+int fdg_gauss_reset_status(fdg_gauss_t *g, void *stream);
+int fdg_gauss_read_status(fdg_gauss_t *g, fdg_status_t *out, void *stream);
+
 /* halo helper: out[i][m][v] = u[elems[i]][line node m of direction dir at end `side`][v] */
 int fdg_pack_faces(const double *u, const int32_t *elems, int32_t n, int32_t d, int32_t degree, int32_t dir,
                    int32_t side, double *out, void *stream);

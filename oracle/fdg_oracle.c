@@ -642,6 +642,125 @@ int or_rhs_range(const or_mesh *M, const double *u, double *du, int vflux, int s
     return 0;
 }
 
+/* ------------------------------------------------ Gauss-family schemes
+ * Restatement of the reference's scalar gauss path (discretization.py:375-443
+ * _gauss_line_terms with include_corner=False as rhs uses it, :966-995
+ * _scalar_gauss_volume, :839-895 _gauss_surface, :985-995 assembly):
+ * zero-corner hybridized volume term on Gauss nodes with entropy-projected
+ * face states, then the interface fluxes of the projected states lifted
+ * through the dense boundary rows, then -(acc / J). The projection itself
+ * (entropy variables, boundary interpolation, entropy2cons) is numpy in
+ * oracle.py, as in the reference. Tables (operators.py:300-357):
+ *   vv[a*p1+b]   volume pair weight c_ab (pairs a < b, both-zero pairs skipped)
+ *   cvol[s*p1+a] volume-row weight of the (a, face s) crossing
+ *   cface[s*p1+a] face-row weight of the crossing
+ *   lift[s*p1+a] R[s][a] / w[a]  (side 1: lift_m, side 0: lift_p)
+ * proj (n_elem, d, 2, fn, nvar) projected face states; nrm (n_elem, d, 2, fn, d)
+ * each element's own face metric traces (the volume crossings); fnrm
+ * (n_elem, d, fn, d) the interface normals face_ja (NULL: nrm side 1).     */
+typedef struct {
+    const double *vv, *cvol, *cface, *lift;
+} or_gauss_tables;
+
+static void gauss_element(const or_mesh *M, const or_gauss_tables *T, int64_t e, const double *u,
+                          const double *proj, const double *nrm, const double *fnrm, double *du, int vflux,
+                          int sflux, node_t *q, double *acc)
+{
+    const int d = M->d, p1 = M->p1, nvar = d + 2, nn = ipow(p1, d), fn = ipow(p1, d - 1);
+    const double gm1 = M->gamma - 1.0;
+    for (int i = 0; i < nn; ++i) make_node(&q[i], u + (e * nn + i) * nvar, d, gm1, vflux, PRE_NONE);
+    for (int i = 0; i < nn * nvar; ++i) acc[i] = 0.0;
+    const double *ja = M->ja + e * nn * d * d;
+    double f[5], alpha[3];
+    for (int n = 0; n < d; ++n) {
+        for (int m = 0; m < fn; ++m) {
+            for (int a = 0; a < p1; ++a)
+                for (int b = a + 1; b < p1; ++b) {
+                    const double cab = T->vv[a * p1 + b], cba = T->vv[b * p1 + a];
+                    if (cab == 0.0 && cba == 0.0) continue;
+                    const int i = line_node(d, p1, n, m, a), k = line_node(d, p1, n, m, b);
+                    for (int j = 0; j < d; ++j) alpha[j] = 0.5 * (ja[(i * d + n) * d + j] + ja[(k * d + n) * d + j]);
+                    two_point(vflux, PRE_NONE, &q[i], &q[k], alpha, -1, d, M->gamma, M->igm1, f);
+                    for (int v = 0; v < nvar; ++v) {
+                        acc[i * nvar + v] += cab * f[v];
+                        acc[k * nvar + v] += cba * f[v];
+                    }
+                }
+            for (int s = 0; s < 2; ++s) {
+                const double *fs = proj + ((((e * d + n) * 2 + s) * fn) + m) * nvar;
+                const double *fj = nrm + ((((e * d + n) * 2 + s) * fn) + m) * d;
+                node_t fq;
+                make_node(&fq, fs, d, gm1, vflux, PRE_NONE);
+                double rface[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                for (int a = 0; a < p1; ++a) {
+                    const int i = line_node(d, p1, n, m, a);
+                    for (int j = 0; j < d; ++j) alpha[j] = 0.5 * (ja[(i * d + n) * d + j] + fj[j]);
+                    two_point(vflux, PRE_NONE, &q[i], &fq, alpha, -1, d, M->gamma, M->igm1, f);
+                    const double ca = T->cvol[s * p1 + a], cf = T->cface[s * p1 + a];
+                    for (int v = 0; v < nvar; ++v) {
+                        acc[i * nvar + v] += ca * f[v];
+                        rface[v] += cf * f[v];
+                    }
+                }
+                for (int a = 0; a < p1; ++a) {
+                    const double la = T->lift[s * p1 + a];
+                    if (la == 0.0) continue;
+                    const int i = line_node(d, p1, n, m, a);
+                    for (int v = 0; v < nvar; ++v) acc[i * nvar + v] += la * rface[v];
+                }
+            }
+        }
+    }
+    /* interfaces: as minus element (+= lift_m F) of face (e, +n) and as plus
+     * element (-= lift_p F) of face (minus(e), +n), in the reference's face
+     * loop order (faces ascending) */
+    for (int n = 0; n < d; ++n) {
+        const int64_t ep = M->plus[n * M->n_elem + e], em = M->minus[n * M->n_elem + e];
+        for (int pass = 0; pass < 2; ++pass) {
+            const int as_plus = (em < e) ? (pass == 0) : (pass == 1);
+            const int64_t owner = as_plus ? em : e, other = as_plus ? e : ep;
+            for (int m = 0; m < fn; ++m) {
+                const double *ul = proj + ((((owner * d + n) * 2 + 1) * fn) + m) * nvar;
+                const double *ur = proj + ((((other * d + n) * 2 + 0) * fn) + m) * nvar;
+                const double *nr = fnrm ? fnrm + (((owner * d + n) * fn) + m) * d
+                                        : nrm + ((((owner * d + n) * 2 + 1) * fn) + m) * d;
+                node_t l, r;
+                make_node(&l, ul, d, gm1, sflux, PRE_NONE);
+                make_node(&r, ur, d, gm1, sflux, PRE_NONE);
+                two_point(sflux, PRE_NONE, &l, &r, nr, -1, d, M->gamma, M->igm1, f);
+                for (int a = 0; a < p1; ++a) {
+                    const double la = T->lift[(as_plus ? 0 : 1) * p1 + a];
+                    if (la == 0.0) continue;
+                    const int i = line_node(d, p1, n, m, a);
+                    for (int v = 0; v < nvar; ++v) {
+                        if (as_plus) acc[i * nvar + v] -= la * f[v];
+                        else acc[i * nvar + v] += la * f[v];
+                    }
+                }
+            }
+        }
+    }
+    for (int i = 0; i < nn; ++i) {
+        const double J = M->jac[e * nn + i];
+        for (int v = 0; v < nvar; ++v) {
+            const double t = acc[i * nvar + v] / J;
+            du[(e * nn + i) * nvar + v] = -t;
+        }
+    }
+}
+
+int or_gauss_rhs(const or_mesh *M, const or_gauss_tables *T, const double *u, const double *proj,
+                 const double *nrm, const double *fnrm, double *du, int vflux, int sflux)
+{
+    const int nn = ipow(M->p1, M->d), nvar = M->d + 2;
+    node_t *q = (node_t *)malloc(sizeof(node_t) * nn);
+    double *acc = (double *)malloc(sizeof(double) * nn * nvar);
+    for (int64_t e = 0; e < M->n_elem; ++e) gauss_element(M, T, e, u, proj, nrm, fnrm, du, vflux, sflux, q, acc);
+    free(q);
+    free(acc);
+    return 0;
+}
+
 /* single two-point flux evaluation (conserved input), for property tests */
 int or_two_point(int d, int flux, int pre, double gamma, double igm1, const double *ul,
                  const double *ur, const double *nrm, int cart_axis, double *f)

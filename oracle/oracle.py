@@ -72,6 +72,10 @@ class OrMesh(ctypes.Structure):
     ]
 
 
+class OrGaussTables(ctypes.Structure):
+    _fields_ = [("vv", ctypes.c_void_p), ("cvol", ctypes.c_void_p), ("cface", ctypes.c_void_p), ("lift", ctypes.c_void_p)]
+
+
 _libs = {}
 
 
@@ -97,6 +101,7 @@ def lib(variant="glibc"):
         L.or_rhs_range.argtypes = [P, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int]
         L.or_gate.argtypes = [P, vp, vp, vp]
+        L.or_gauss_rhs.argtypes = [P, ctypes.POINTER(OrGaussTables), vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
         L.or_gate.restype = ctypes.c_int64
         L.or_two_point.argtypes = [
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -364,3 +369,145 @@ def stable_dt(u, setup, cfl=0.5, gamma=1.4):
     lam = np.sqrt(np.sum(v * v, axis=-1)) + np.sqrt(gamma * p / rho)
     scale = np.asarray(setup.metrics.jac) ** (1.0 / d)
     return cfl * float(np.min(scale / (lam * (2 * setup.op.degree + 1))))
+
+
+# ------------------------------------------------------- Gauss-family schemes
+# numpy restatement of the reference's entropy projection and scatter tables
+# (test infrastructure; pinned against tests/golden/gauss_*.npz written by the
+# reference itself, tests/test_oracle.py). The element loop is C (or_gauss_rhs).
+
+_FACE_N = (-1.0, 1.0)
+
+
+def gauss_tables(op, scheme):
+    """(vv, cvol, cface, lift) of operators.py:300-357 in float, from the
+    operator's own arrays: the hybridized skew operator
+    Q_h = [[skew(M D), R^T N / 2], [-N R / 2, N / 2]] gives the volume pair
+    weights 2 Q[a,b] / w_a (gauss_fluxdiff) -- or the split-derivative
+    matrix 2D - M^-1 R^T B N R (gauss_surface_correction) -- the crossing
+    weights 2 Q[a, face] / w_a and 2 Q[face, a], and the lift R[s] / w."""
+    w = np.asarray(op.weights, dtype=np.float64)
+    D = np.asarray(op.D, dtype=np.float64)
+    R = np.asarray(op.boundary_interp, dtype=np.float64)
+    n = w.shape[0]
+    nf = np.array(_FACE_N)
+    md = w[:, None] * D
+    q = np.zeros((n + 2, n + 2))
+    q[:n, :n] = 0.5 * (md - md.T)
+    q[:n, n:] = 0.5 * (R.T * nf[None, :])
+    q[n:, :n] = -0.5 * (nf[:, None] * R)
+    q[n:, n:] = 0.5 * np.diag(nf)
+    vv = np.zeros((n, n))
+    if scheme == "gauss_surface_correction":
+        mat = 2.0 * D - (R.T @ (nf[:, None] * R)) / w[:, None]
+        for a in range(n):
+            for b in range(a + 1, n):
+                if mat[a, b] != 0.0 or mat[b, a] != 0.0:
+                    vv[a, b], vv[b, a] = float(mat[a, b]), float(mat[b, a])
+    else:
+        for a in range(n):
+            for b in range(a + 1, n):
+                if q[a, b] != 0.0 or q[b, a] != 0.0:
+                    vv[a, b], vv[b, a] = float(2.0 * q[a, b] / w[a]), float(2.0 * q[b, a] / w[b])
+    cvol = np.array([[float(2.0 * q[a, n + s] / w[a]) for a in range(n)] for s in (0, 1)])
+    cface = np.array([[float(2.0 * q[n + s, a]) for a in range(n)] for s in (0, 1)])
+    lift = np.array([[float(R[s, a] / w[a]) for a in range(n)] for s in (0, 1)])
+    return vv, cvol, cface, lift
+
+
+def gauss_project(u, op, gamma=1.4):
+    """Entropy-projected face states (n_elem, d, 2, fn, nvar) as
+    discretization._project_all computes them (entropy variables, boundary
+    interpolation along each direction, entropy2cons); None entries if a face
+    state is inadmissible (the caller raises)."""
+    u = np.asarray(u, dtype=np.float64)
+    n_elem, nn, nvar = u.shape
+    d = nvar - 2
+    p1 = round(nn ** (1.0 / d))
+    w = entropy_vars(u, gamma)
+    w_nd = w.reshape((n_elem,) + (p1,) * d + (nvar,))
+    fn = p1 ** (d - 1)
+    out = np.empty((n_elem, d, 2, fn, nvar))
+    R = np.asarray(op.boundary_interp, dtype=np.float64)
+    for n in range(d):
+        moved = np.moveaxis(w_nd, n + 1, -2)
+        for side in (0, 1):
+            wf = np.einsum("...kv,k->...v", moved, R[side]).reshape(n_elem, -1, nvar)
+            out[:, n, side] = entropy2cons(wf, gamma)
+    return out
+
+
+def entropy2cons(w, gamma):
+    """euler.py:149-170."""
+    d = w.shape[-1] - 2
+    b = -w[..., d + 1]
+    if not np.all(b > 0.0):
+        raise OracleAdmissibilityError("entropy2cons: last entropy variable must be negative (min -w=%r)"
+                                       % float(np.min(b)))
+    v = w[..., 1 : d + 1] / b[..., None]
+    s = gamma - (gamma - 1.0) * (w[..., 0] + 0.5 * b * np.sum(v * v, axis=-1))
+    p = np.exp((s + gamma * np.log(b)) / (1.0 - gamma))
+    rho = b * p
+    out = np.empty_like(w)
+    out[..., 0] = rho
+    out[..., 1 : d + 1] = rho[..., None] * v
+    out[..., d + 1] = p * (1.0 / (gamma - 1.0)) + 0.5 * rho * np.sum(v * v, axis=-1)
+    return out
+
+
+def gauss_face_traces(ja, op, d):
+    """Each element's own metric traces (n_elem, d, 2, fn, d) as
+    discretization._own_face_ja computes them per element (einsum)."""
+    ja = np.asarray(ja, dtype=np.float64)
+    n_elem, nn = ja.shape[:2]
+    p1 = round(nn ** (1.0 / d))
+    R = np.asarray(op.boundary_interp, dtype=np.float64)
+    out = np.empty((n_elem, d, 2, p1 ** (d - 1), d))
+    for e in range(n_elem):
+        nd = ja[e].reshape((p1,) * d + (d, d))
+        for n in range(d):
+            field = np.moveaxis(nd[..., n, :], n, -2)
+            for s in (0, 1):
+                out[e, n, s] = np.einsum("...kj,k->...j", field, R[s]).reshape(-1, d)
+    return out
+
+
+def gauss_rhs(u, setup, scheme, volume_flux, surface_flux, proj=None, nrm=None, fnrm=None, variant="glibc"):
+    """du of rhs(u, setup, RhsConfig(volume_scheme=scheme, ...)) on Gauss
+    operators (discretization.py:976-995, the scalar path). ``setup``:
+    d, op, gas, metrics.{ja, jac[, face_ja]}, plus_neighbor."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    d = setup.d
+    gamma = setup.gas.gamma
+    bad = gate(u, _gauss_mesh(setup, u.shape[0]))
+    if bad is not None:
+        e, i, rho, p = bad
+        raise OracleAdmissibilityError("inadmissible state at element %d, node %d: rho=%r, p=%r" % (e, i, rho, p))
+    if proj is None:
+        proj = gauss_project(u, setup.op, gamma)
+    if nrm is None:
+        nrm = gauss_face_traces(setup.metrics.ja, setup.op, d)
+    if fnrm is None and getattr(setup.metrics, "face_ja", None) is not None:
+        fnrm = np.stack([np.asarray(setup.metrics.face_ja[n]) for n in range(d)], axis=1)
+    vv, cvol, cface, lift = (np.ascontiguousarray(t) for t in gauss_tables(setup.op, scheme))
+    tab = OrGaussTables(vv.ctypes.data, cvol.ctypes.data, cface.ctypes.data, lift.ctypes.data)
+    m = _gauss_mesh(setup, u.shape[0])
+    proj = np.ascontiguousarray(proj)
+    nrm = np.ascontiguousarray(nrm)
+    fnrm = None if fnrm is None else np.ascontiguousarray(fnrm)
+    du = np.empty_like(u)
+    lib(variant).or_gauss_rhs(ctypes.byref(m.struct), ctypes.byref(tab), _ptr(u), _ptr(proj), _ptr(nrm), _ptr(fnrm),
+                              _ptr(du), FLUX_IDS[volume_flux], FLUX_IDS[surface_flux])
+    return du
+
+
+def _gauss_mesh(setup, n_elem):
+    d = setup.d
+    plus = np.stack([np.asarray(setup.plus_neighbor[n]) for n in range(d)])
+    minus = np.empty_like(plus)
+    for n in range(d):
+        minus[n, plus[n]] = np.arange(n_elem)
+    w = np.asarray(setup.op.weights)
+    return MeshArrays(d, w.shape[0], n_elem, np.zeros((w.shape[0], w.shape[0])), w, setup.gas.gamma,
+                      setup.gas.inv_gamma_minus_one, False, None, 0.0, np.asarray(setup.metrics.ja),
+                      np.asarray(setup.metrics.jac), plus, minus)

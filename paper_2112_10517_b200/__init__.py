@@ -34,7 +34,7 @@ from .errors import (
 from .euler import GasParams, cons2prim, prim2cons
 from .fluxes import FluxCounter, count_guard
 from .geometry import StructuredMesh, build_mesh, compute_metrics
-from .operators import build_dsplit, lgl_operator, make_operator, node_lines, pair_table
+from .operators import build_dsplit, gauss_operator, gauss_scatter_tables, lgl_operator, make_operator, node_lines, pair_table
 from .timeint import RK54, SSPRK43, DeviceStepper, RKMethod, ShuOsherMethod, StepController, integrate, rk_step, stable_dt
 
 __version__ = "0.1.0"

@@ -61,6 +61,25 @@ class GeometryDesc(ctypes.Structure):
     ]
 
 
+class GaussDesc(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("degree", ctypes.c_int32),
+        ("n_elem", ctypes.c_int64),
+        ("gamma", ctypes.c_double),
+        ("inv_gamma_minus_one", ctypes.c_double),
+        ("boundary_interp", ctypes.c_void_p),
+        ("vv", ctypes.c_void_p),
+        ("cvol", ctypes.c_void_p),
+        ("cface", ctypes.c_void_p),
+        ("lift", ctypes.c_void_p),
+        ("ja", ctypes.c_void_p),
+        ("jac", ctypes.c_void_p),
+        ("plus", ctypes.c_void_p),
+        ("minus", ctypes.c_void_p),
+    ]
+
+
 class Scheme(ctypes.Structure):
     _fields_ = [
         ("volume_flux", ctypes.c_int32),
@@ -108,6 +127,13 @@ EXPORTS = (
     "fdg_mesh_set_reserve_sms",
     "fdg_pack_faces",
     "fdg_fp64_probe",
+    "fdg_gauss_create",
+    "fdg_gauss_destroy",
+    "fdg_gauss_project",
+    "fdg_gauss_rhs",
+    "fdg_gauss_gate",
+    "fdg_gauss_reset_status",
+    "fdg_gauss_read_status",
 )
 
 _lib = None
@@ -154,6 +180,13 @@ def lib():
     L.fdg_diagnostic.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fdg_pack_faces.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp]
     L.fdg_fp64_probe.argtypes = [P(ctypes.c_double), vp]
+    L.fdg_gauss_create.argtypes = [P(GaussDesc), P(vp)]
+    L.fdg_gauss_destroy.argtypes = [vp]
+    L.fdg_gauss_project.argtypes = [vp, vp, vp, vp, vp]
+    L.fdg_gauss_rhs.argtypes = [vp, P(Scheme), vp, vp, vp, vp, vp, vp]
+    L.fdg_gauss_gate.argtypes = [vp, vp, vp]
+    L.fdg_gauss_reset_status.argtypes = [vp, vp]
+    L.fdg_gauss_read_status.argtypes = [vp, P(StatusRec), vp]
     if L.fdg_abi_version() != 1:
         raise NativeLibraryError("libfdg.so ABI version %d, expected 1" % L.fdg_abi_version())
     _lib = L

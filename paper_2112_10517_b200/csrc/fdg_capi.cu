@@ -64,6 +64,9 @@ static const char* flux_name(int k)
 
 extern "C" {
 
+// error reporting for the other translation units (fdg_gauss.cu)
+int fdg_internal_fail(int rc, const char* msg) { return fail(rc, "%s", msg); }
+
 int fdg_abi_version(void) { return FDG_ABI_VERSION; }
 
 const char* fdg_last_error(void) { return g_last_error.c_str(); }

@@ -331,6 +331,125 @@ class DeviceMesh:
         )
 
 
+class GaussDeviceMesh:
+    """Device image of a Gauss-family setup for one scheme (its scatter
+    tables, operators.gauss_scatter_tables) and the libfdg gauss handle
+    (fdg_gauss_*): metric terms at the Gauss nodes, neighbour tables, and the
+    library-owned projection scratch. Duck-typed setup: d, op.{weights, D,
+    boundary_interp, degree}, metrics.{ja, jac}, plus_neighbor, gas."""
+
+    def __init__(self, setup, scheme, device=None):
+        from .operators import gauss_scatter_tables
+
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        self.d = int(setup.d)
+        op = setup.op
+        self.degree = int(op.degree)
+        self.p1 = self.degree + 1
+        self.nn = self.p1**self.d
+        self.nvar = self.d + 2
+        self.fn = self.p1 ** (self.d - 1)
+        self.gamma = float(setup.gas.gamma)
+        plus = np.stack([np.asarray(setup.plus_neighbor[n], dtype=np.int64) for n in range(self.d)])
+        self.n_elem = n_elem = plus.shape[1]
+        self.elem_lo = 0
+        minus = np.empty_like(plus)
+        for n in range(self.d):
+            minus[n, plus[n]] = np.arange(n_elem)
+        dev = self.device
+        self.plus = torch.as_tensor(plus.astype(np.int32), device=dev).contiguous()
+        self.minus = torch.as_tensor(minus.astype(np.int32), device=dev).contiguous()
+        ja, jac = setup.metrics.ja, setup.metrics.jac
+        if isinstance(ja, torch.Tensor):
+            self.ja, self.jac = ja.to(dev).contiguous(), jac.to(dev).contiguous()
+        else:
+            self.ja = torch.as_tensor(np.ascontiguousarray(np.asarray(ja, dtype=np.float64)), device=dev)
+            self.jac = torch.as_tensor(np.ascontiguousarray(np.asarray(jac, dtype=np.float64)), device=dev)
+        tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in gauss_scatter_tables(op, scheme)]
+        R = np.ascontiguousarray(np.asarray(op.boundary_interp, dtype=np.float64))
+        self._host_keep = (tabs, R)
+        desc = N.GaussDesc()
+        desc.d, desc.degree, desc.n_elem = self.d, self.degree, n_elem
+        desc.gamma, desc.inv_gamma_minus_one = float(setup.gas.gamma), float(setup.gas.inv_gamma_minus_one)
+        desc.boundary_interp = R.ctypes.data
+        desc.vv, desc.cvol, desc.cface, desc.lift = (t.ctypes.data for t in tabs)
+        desc.ja, desc.jac = self.ja.data_ptr(), self.jac.data_ptr()
+        desc.plus, desc.minus = self.plus.data_ptr(), self.minus.data_ptr()
+        handle = ctypes.c_void_p()
+        N.check(N.lib().fdg_gauss_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self.handle = handle
+        self._finalizer = weakref.finalize(self, N.lib().fdg_gauss_destroy, handle)
+        self._staging = {}
+
+    @property
+    def shape(self):
+        return (self.n_elem, self.nn, self.nvar)
+
+    def empty(self):
+        return self.torch.empty(self.shape, dtype=self.torch.float64, device=self.device)
+
+    def staging(self, key, shape):
+        buf = self._staging.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = N.pinned_empty(shape)
+            self._staging[key] = buf
+        return buf
+
+    def proj_shape(self):
+        return (self.n_elem, self.d, 2, self.fn, self.nvar)
+
+    def nrm_shape(self):
+        return (self.n_elem, self.d, 2, self.fn, self.d)
+
+    def project(self, u, proj=None, nrm=None, stream=None):
+        torch = self.torch
+        proj = proj if proj is not None else torch.empty(self.proj_shape(), dtype=torch.float64, device=self.device)
+        nrm = nrm if nrm is not None else torch.empty(self.nrm_shape(), dtype=torch.float64, device=self.device)
+        N.check(N.lib().fdg_gauss_project(self.handle, _ptr(u), _ptr(proj), _ptr(nrm), _stream_handle(stream)))
+        return proj, nrm
+
+    def rhs(self, u, scheme, out=None, proj=None, nrm=None, fnrm=None, stream=None):
+        out = self.empty() if out is None else out
+        N.check(N.lib().fdg_gauss_rhs(self.handle, ctypes.byref(scheme), _ptr(u), _ptr(proj), _ptr(nrm), _ptr(fnrm),
+                                      _ptr(out), _stream_handle(stream)))
+        return out
+
+    def gate(self, u, stream=None):
+        N.check(N.lib().fdg_gauss_gate(self.handle, _ptr(u), _stream_handle(stream)))
+
+    def reset_status(self, stream=None):
+        N.check(N.lib().fdg_gauss_reset_status(self.handle, _stream_handle(stream)))
+
+    def read_status(self, stream=None):
+        rec = N.StatusRec()
+        N.check(N.lib().fdg_gauss_read_status(self.handle, ctypes.byref(rec), _stream_handle(stream)))
+        return int(rec.first_bad), int(rec.bad_stage)
+
+    raise_if_inadmissible = DeviceMesh.raise_if_inadmissible
+
+
+_GAUSS_CACHE = {}
+
+
+def gauss_mesh_for(setup, scheme, device=None):
+    """GaussDeviceMesh cached per (setup object, scheme); dropped with the setup."""
+    key = (id(setup), scheme, str(device))
+    hit = _GAUSS_CACHE.get(key)
+    if hit is not None and hit[0]() is setup:
+        return hit[1]
+    gm = GaussDeviceMesh(setup, scheme, device=device)
+    try:
+        ref = weakref.ref(setup)
+        weakref.finalize(setup, lambda k=key, r=ref: _GAUSS_CACHE.pop(k, None) if _GAUSS_CACHE.get(k, (None,))[0] is r
+                         else None)
+    except TypeError:
+        ref = (lambda s: (lambda: s))(setup)
+    _GAUSS_CACHE[key] = (ref, gm)
+    return gm
+
+
 _CACHE = {}
 
 
@@ -362,6 +481,7 @@ def _evict(key, ref):
 def clear_cache():
     """Drop every cached DeviceMesh (their device memory is freed once unreferenced)."""
     _CACHE.clear()
+    _GAUSS_CACHE.clear()
 
 
-__all__ = ["DeviceMesh", "device_mesh_for", "scheme_struct", "DivergenceError"]
+__all__ = ["DeviceMesh", "GaussDeviceMesh", "device_mesh_for", "gauss_mesh_for", "scheme_struct", "DivergenceError"]

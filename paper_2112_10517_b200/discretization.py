@@ -29,12 +29,13 @@ from .errors import AdmissibilityError, ConfigurationError, UnsupportedOperatorE
 from .geometry import compute_metrics, element_coords, neighbor_table
 from .operators import build_dsplit, node_lines, pair_table
 
-VOLUME_SCHEMES = ("fluxdiff",)
+VOLUME_SCHEMES = ("fluxdiff", "gauss_fluxdiff", "gauss_surface_correction")
+GAUSS_SCHEMES = ("gauss_fluxdiff", "gauss_surface_correction")
 PRECOMPUTE_MODES = ("none", "primitives", "primitives_and_logs")
 KERNELS = ("reference", "batched")
 VOLUME_KINDS = _fluxes.VOLUME_KINDS
 SURFACE_KINDS = _fluxes.SURFACE_KINDS
-_OUT_OF_SCOPE_SCHEMES = ("strong", "weak", "overintegration", "gauss_fluxdiff", "gauss_surface_correction")
+_OUT_OF_SCOPE_SCHEMES = ("strong", "weak", "overintegration")
 
 
 @dataclass(frozen=True)
@@ -70,9 +71,14 @@ class RhsConfig:
         _fluxes.require_volume_kind(self.volume_flux)
         if setup is not None:
             family = getattr(setup.op, "family", "lgl")
-            if family != "lgl":
+            if self.volume_scheme.startswith("gauss") and family != "gauss":
                 raise ConfigurationError(
-                    "volume_scheme: 'fluxdiff' requires the lgl family (diagonal boundary operator)"
+                    "volume_scheme: %r requires gauss operators, got family %r" % (self.volume_scheme, family)
+                )
+            if self.volume_scheme == "fluxdiff" and family != "lgl":
+                raise ConfigurationError(
+                    "volume_scheme: 'fluxdiff' requires the lgl family (diagonal boundary operator); "
+                    "use the gauss schemes on gauss nodes"
                 )
 
     def scheme(self):
@@ -140,8 +146,10 @@ def build_setup(mesh, op, gas, with_coords=True, device=None):
     ``device`` (extension, e.g. "cuda"): coordinates and curved metrics are
     computed on the GPU (geometry.device_geometry) and held as CUDA tensors,
     so no per-node geometry is built on or copied from the host."""
+    if op.family == "gauss":
+        return _build_gauss_setup(mesh, op, gas, device)
     if op.family != "lgl":
-        raise UnsupportedOperatorError("the flux-differencing setup needs LGL operators, got %r" % (op.family,))
+        raise UnsupportedOperatorError("unknown operator family %r" % (op.family,))
     if device is not None:
         from .geometry import MetricData, device_geometry
 
@@ -162,6 +170,32 @@ def build_setup(mesh, op, gas, with_coords=True, device=None):
         lines=node_lines(op.n_nodes, mesh.d),
         plus_neighbor=neighbor_table(mesh),
         dsplit=build_dsplit(op),
+    )
+
+
+def _build_gauss_setup(mesh, op, gas, device=None):
+    """Setup on Gauss nodes (reference discretization.py:609-657 with a gauss
+    operator): coordinates at the Gauss nodes, per-node metric terms (also on
+    Cartesian meshes: the gauss kernels always take the directional form,
+    as the reference's gauss path does), neighbours; no split matrix."""
+    from .geometry import MetricData, device_geometry
+
+    R = op.boundary_interp
+    if device is not None:
+        coords, ja, jac = device_geometry(mesh, op, device=device, coords=True)
+        if mesh.is_cartesian:
+            m = compute_metrics(mesh, op)
+            ja, jac = m.ja, m.jac
+        metrics = MetricData(mesh.d, op.n_nodes, mesh.n_elements, mesh.is_cartesian, ja=ja, jac=jac,
+                             boundary_interp=R)
+    else:
+        coords = element_coords(mesh, op)
+        m = compute_metrics(mesh, op, coords)
+        metrics = MetricData(mesh.d, op.n_nodes, mesh.n_elements, m.cartesian, areas=m.areas,
+                             jac_const=m.jac_const, ja=m.ja, jac=m.jac, boundary_interp=R)
+    return SpatialSetup(
+        mesh=mesh, op=op, gas=gas, metrics=metrics, coords=coords,
+        lines=node_lines(op.n_nodes, mesh.d), plus_neighbor=neighbor_table(mesh), dsplit=None,
     )
 
 
@@ -391,9 +425,13 @@ def surface_terms(u, setup, surface_flux, subtract_own=False, face_states=None, 
 
 def rhs(u, setup, config, counter=None):
     """du/dt = -(VOL + SURF) (discretization.py:896-949), admissibility gate
-    included (discretization.py:660-672)."""
+    included (discretization.py:660-672). The gauss schemes (volume_scheme
+    "gauss_fluxdiff" / "gauss_surface_correction" on Gauss operators) run
+    fdg_gauss_* (discretization.py:976-995)."""
     config = as_rhs_config(config)
     config.validate(setup)
+    if config.volume_scheme in GAUSS_SCHEMES:
+        return _gauss_rhs(u, setup, config, counter)
     dm = device_mesh_for(setup)
     io = _Io(dm, u)
     dm.reset_status()
@@ -403,6 +441,61 @@ def rhs(u, setup, config, counter=None):
     sc = _surface_counts(setup)
     _count(counter, tp + sc, lm + _surface_logmeans(config.surface_flux, sc))
     return io.finish(res)
+
+
+def _gauss_counts(setup, config):
+    """The reference's counter totals for the gauss path (measured on it):
+    per element line, |pairs| + 2 (p+1) volume evaluations and 2 interface
+    evaluations; two log means per Ranocha / Chandrashekar evaluation."""
+    from .operators import gauss_scatter_tables
+
+    d = setup.d
+    p1 = setup.op.degree + 1
+    vv = gauss_scatter_tables(setup.op, config.volume_scheme)[0]
+    pairs = sum(1 for a in range(p1) for b in range(a + 1, p1) if vv[a, b] != 0.0 or vv[b, a] != 0.0)
+    lines = setup_n_elements(setup) * d * p1 ** (d - 1)
+    vol = lines * (pairs + 2 * p1)
+    surf = 2 * lines
+    logs = ("ranocha", "chandrashekar")
+    return vol + surf, (2 * vol if config.volume_flux in logs else 0) + (2 * surf if config.surface_flux in logs else 0)
+
+
+def _gauss_rhs(u, setup, config, counter):
+    from .device import gauss_mesh_for
+
+    gm = gauss_mesh_for(setup, config.volume_scheme)
+    io = _Io(gm, u)
+    gm.reset_status()
+    gm.gate(io.u)
+    first_bad, _ = gm.read_status()
+    if first_bad >= 0:
+        gm.raise_if_inadmissible(io.u, first_bad, setup.gas.gamma)
+    proj, nrm = gm.project(io.u)
+    res = gm.rhs(io.u, config.scheme(), out=io.device_out(), proj=proj, nrm=nrm)
+    _, bad_face = gm.read_status()
+    if bad_face >= 0:
+        _raise_projection(io.u, setup, bad_face)
+    tp, lm = _gauss_counts(setup, config)
+    _count(counter, tp, lm)
+    return io.finish(res)
+
+
+def _raise_projection(u_dev, setup, code):
+    """The reference's _project_all error (discretization.py:826-836)."""
+    from .euler import entropy_vars
+
+    n, side = divmod(int(code), 2)
+    u = u_dev.double().cpu().numpy()
+    d = u.shape[-1] - 2
+    p1 = setup.op.degree + 1
+    w = entropy_vars(u, setup.gas).reshape((u.shape[0],) + (p1,) * d + (d + 2,))
+    row = np.asarray(setup.op.boundary_interp)[side]
+    wf = np.tensordot(np.moveaxis(w, n + 1, -2), row, axes=([-2], [0]))
+    b = -wf[..., d + 1]
+    raise AdmissibilityError(
+        "entropy projection produced an inadmissible face state (direction %d, side %d): "
+        "entropy2cons: last entropy variable must be negative (min -w=%r)" % (n, side, float(np.min(b)))
+    )
 
 
 class _ElementSetup:

@@ -162,13 +162,17 @@ class MetricData:
     own Ja^n (for LGL a restriction: geometry.py:311-326 of the reference).
     """
 
-    def __init__(self, d, p1, n_elem, cartesian, areas=None, jac_const=None, ja=None, jac=None):
+    def __init__(self, d, p1, n_elem, cartesian, areas=None, jac_const=None, ja=None, jac=None, boundary_interp=None):
         self.d, self.p1, self.n_elem = d, p1, n_elem
         self.cartesian = bool(cartesian)
         self.areas = None if areas is None else tuple(float(a) for a in areas)
         self.jac_const = None if jac_const is None else float(jac_const)
         self._ja, self._jac = ja, jac
         self._face_ja = None
+        self._elem_face_ja = None
+        # Gauss nodes have no boundary node: face traces are extrapolations
+        # with the boundary rows R (reference geometry.py:253-262, 311-326)
+        self.boundary_interp = None if boundary_interp is None else np.asarray(boundary_interp, dtype=np.float64)
 
     @property
     def nn(self):
@@ -190,7 +194,29 @@ class MetricData:
         return self._jac
 
     @property
+    def elem_face_ja(self):
+        """elem_face_ja[n][e, s, m, :]: element e's own trace of its Ja^n on
+        side s (0: the -1 face, 1: the +1 face) at face node m."""
+        if self._elem_face_ja is None:
+            from .operators import node_lines
+
+            lines = node_lines(self.p1, self.d)
+            ja = np.asarray(self.ja)
+            out = []
+            for n in range(self.d):
+                vals = ja[:, lines[n], n, :]  # (n_elem, fn, p1, d)
+                if self.boundary_interp is None:
+                    sides = [vals[:, :, 0, :], vals[:, :, -1, :]]
+                else:
+                    sides = [np.einsum("efkj,k->efj", vals, self.boundary_interp[s]) for s in (0, 1)]
+                out.append(np.ascontiguousarray(np.stack(sides, axis=1)))
+            self._elem_face_ja = tuple(out)
+        return self._elem_face_ja
+
+    @property
     def face_ja(self):
+        if self._face_ja is None and self.boundary_interp is not None:
+            self._face_ja = tuple(np.ascontiguousarray(t[:, 1]) for t in self.elem_face_ja)
         if self._face_ja is None:
             from .operators import node_lines
 

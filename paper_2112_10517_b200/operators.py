@@ -249,3 +249,63 @@ def pair_table(mat):
     ia, ib = np.triu_indices(m.shape[0], k=1)
     keep = (m[ia, ib] != 0.0) | (m[ib, ia] != 0.0)
     return tuple((int(a), int(b), float(m[a, b]), float(m[b, a])) for a, b in zip(ia[keep], ib[keep]))
+
+
+# ------------------------------------------------------ Gauss-family tables
+
+_FACE_SIGN = (-1.0, 1.0)
+GAUSS_SCHEMES = ("gauss_fluxdiff", "gauss_surface_correction")
+
+
+def hybridized_skew(op):
+    """The hybridized skew operator on [volume nodes; -1 face; +1 face]
+    (reference operators.py:220-245, build_hybridized):
+    Q_h = [[ (M D - (M D)^T)/2,  R^T N / 2 ],
+           [ -N R / 2,           N / 2     ]]
+    so Q_h + Q_h^T = blockdiag(0, N) and the face consistency flux lives in
+    the volume operator."""
+    w = np.asarray(op.weights, dtype=np.float64)
+    D = np.asarray(op.D, dtype=np.float64)
+    R = np.asarray(op.boundary_interp, dtype=np.float64)
+    n = w.shape[0]
+    sgn = np.array(_FACE_SIGN)
+    md = w[:, None] * D
+    q = np.zeros((n + 2, n + 2))
+    q[:n, :n] = 0.5 * (md - md.T)
+    q[:n, n:] = 0.5 * (R.T * sgn[None, :])
+    q[n:, :n] = -0.5 * (sgn[:, None] * R)
+    q[n:, n:] = 0.5 * np.diag(sgn)
+    return q
+
+
+def gauss_scatter_tables(op, scheme):
+    """Per-line scatter coefficients of the Gauss schemes (reference
+    operators.py:300-357, hybridized_scatter / skew_pair_table), evaluated in
+    float from the operator's own arrays:
+
+    * vv (p+1, p+1): volume pair weights, vv[a, b] = c_ab for the pair (a, b):
+      2 Q_h[a, b] / w_a ("gauss_fluxdiff") or the split-derivative matrix
+      2D - M^-1 R^T B N R ("gauss_surface_correction"); both-zero pairs are 0
+    * cvol (2, p+1): crossing weight into volume row a, 2 Q_h[a, face s] / w_a
+    * cface (2, p+1): crossing weight into the face row, 2 Q_h[face s, a]
+    * lift (2, p+1): R[s, a] / w_a (carries a face row back to the line)."""
+    if scheme not in GAUSS_SCHEMES:
+        raise UnsupportedOperatorError("unknown gauss scheme %r" % (scheme,))
+    w = np.asarray(op.weights, dtype=np.float64)
+    R = np.asarray(op.boundary_interp, dtype=np.float64)
+    n = w.shape[0]
+    q = hybridized_skew(op)
+    if scheme == "gauss_surface_correction":
+        sgn = np.array(_FACE_SIGN)
+        mat = 2.0 * np.asarray(op.D, dtype=np.float64) - (R.T @ (sgn[:, None] * R)) / w[:, None]
+        vv = np.where(np.eye(n, dtype=bool), 0.0, mat)
+    else:
+        vv = np.zeros((n, n))
+        for a in range(n):
+            for b in range(n):
+                if a != b:
+                    vv[a, b] = 2.0 * q[a, b] / w[a]
+    cvol = np.array([[2.0 * q[a, n + s] / w[a] for a in range(n)] for s in (0, 1)])
+    cface = np.array([[2.0 * q[n + s, a] for a in range(n)] for s in (0, 1)])
+    lift = np.array([[R[s, a] / w[a] for a in range(n)] for s in (0, 1)])
+    return vv, cvol, cface, lift

@@ -81,3 +81,33 @@ def golden_setup(name, gamma=1.4):
 def states(name):
     c = case(name)
     return [k[2:] for k in c if k.startswith("u_")]
+
+
+GAUSS_CASES = ["g2d_cart_p3", "g2d_curv_p3", "g3d_cart_p2", "g3d_curv_p3"]
+
+
+@functools.lru_cache(maxsize=None)
+def gauss_case(name):
+    return dict(np.load(os.path.join(GOLDEN, "gauss_%s.npz" % name)))
+
+
+def gauss_setup(name, gamma=1.4):
+    """Duck-typed Gauss-family setup from the reference's recorded arrays."""
+    from paper_2112_10517_b200.operators import Operator1D
+
+    c = gauss_case(name)
+    p = int(c["p"])
+    d = len(c["dims"])
+    gas = SimpleNamespace(gamma=gamma, inv_gamma_minus_one=1.0 / (gamma - 1.0))
+    op = Operator1D(p, "gauss", c["nodes"], c["weights"], c["D"], c["R"])
+    return SimpleNamespace(
+        d=d, op=op, gas=gas, dsplit=None,
+        metrics=SimpleNamespace(
+            ja=c["ja"], jac=c["jac"], cartesian=bool(c["cartesian"]),
+            face_ja=tuple(c["face_ja_%d" % n] for n in range(d)),
+            elem_face_ja=tuple(c["elem_face_ja_%d" % n] for n in range(d)),
+        ),
+        plus_neighbor=tuple(c["plus_%d" % n] for n in range(d)),
+        n_elements=c["ja"].shape[0], n_nodes=c["ja"].shape[1],
+        mesh=SimpleNamespace(dims=tuple(int(x) for x in c["dims"]), d=d),
+    )

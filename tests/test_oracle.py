@@ -200,3 +200,62 @@ def test_cfg5_sample_oracle_pinned():
     u0, areas, jac = workloads.cartesian_sample(5, 1, op=G.golden_operator(3))
     assert np.array_equal(u0[0], u[0])
     assert jac == float(g["jac"]) and areas[0] == float(g["area"])
+
+
+# ------------------------------------------------------ Gauss-family oracle
+
+
+@pytest.mark.parametrize("name", G.GAUSS_CASES)
+def test_gauss_oracle_bitwise(name):
+    """oracle.gauss_project (numpy, as _project_all) and or_gauss_rhs (C, as
+    the scalar gauss path) against the reference's own outputs
+    (tests/golden/make_gauss.py): BITWISE for every scheme and flux pair."""
+    c = G.gauss_case(name)
+    st = G.gauss_setup(name)
+    d = st.d
+    for sname in ("rand", "wave"):
+        u = c["u_" + sname]
+        proj = oracle.gauss_project(u, st.op)
+        want_proj = np.stack([np.stack([c["proj_%s_%d_%d" % (sname, n, s)] for s in (0, 1)], axis=1)
+                              for n in range(d)], axis=1)
+        assert np.array_equal(proj, want_proj), sname
+        for key in c:
+            if not key.startswith("rhs_%s_" % sname):
+                continue
+            rest = key[len("rhs_%s_" % sname):]
+            scheme = "gauss_surface_correction" if rest.startswith("gauss_surface_correction") else "gauss_fluxdiff"
+            vf, sf = rest[len(scheme) + 1:].split("_")
+            du = oracle.gauss_rhs(u, st, scheme, vf, sf)
+            assert np.array_equal(du, c[key]), key
+
+
+def test_gauss_scatter_tables_match_oracle():
+    from paper_2112_10517_b200.operators import gauss_scatter_tables
+
+    for name in G.GAUSS_CASES:
+        st = G.gauss_setup(name)
+        for scheme in ("gauss_fluxdiff", "gauss_surface_correction"):
+            mine = gauss_scatter_tables(st.op, scheme)
+            ref = oracle.gauss_tables(st.op, scheme)
+            assert all(np.array_equal(a, b) for a, b in zip(mine, ref)), (name, scheme)
+
+
+def test_gauss_counter_totals_match_reference():
+    """Analytic counter totals of the gauss path (discretization._gauss_counts)
+    against the reference's FluxCounter on the same call."""
+    from types import SimpleNamespace
+
+    from paper_2112_10517_b200.discretization import _gauss_counts
+
+    for name in G.GAUSS_CASES:
+        c = G.gauss_case(name)
+        st = G.gauss_setup(name)
+        for key in c:
+            if not key.startswith("counts_rand_"):
+                continue
+            rest = key[len("counts_rand_"):]
+            scheme = "gauss_surface_correction" if rest.startswith("gauss_surface_correction") else "gauss_fluxdiff"
+            vf, sf = rest[len(scheme) + 1:].split("_")
+            cfg = SimpleNamespace(volume_scheme=scheme, volume_flux=vf, surface_flux=sf)
+            tp, lm = _gauss_counts(st, cfg)
+            assert (tp, 0, lm) == tuple(int(x) for x in c[key]), key
