@@ -642,6 +642,75 @@ def measure_sharded(kind, args, rank, world, local, dist):
     }
 
 
+def measure_pid(args):
+    """The paper's own PID protocol (harness.measure_pid):
+    3D isentropic vortex, N=3, 8^3 elements on [-5,5]^3, Ranocha volume and
+    surface flux, RK54 with the CFL step of the initial state, 90 steps = 450
+    RHS evaluations, 5 repeats; FAST fused stage kernels, the 90 steps as one
+    CUDA graph. Also the C oracle's single-thread PID of one RHS (the
+    reference is single-threaded by design, harness.py:449-451)."""
+    from oracle import oracle
+    from paper_2112_10517_b200.pid import build_pid_run, measure_pid_device
+
+    setup, u0, cfg = build_pid_run(d=3, p=3, elements=8, volume_flux="ranocha", surface_flux="ranocha",
+                                   kernel="batched")
+    r = measure_pid_device(setup, u0, cfg, n_steps=90, repeats=5)
+    mesh = oracle.mesh_from_setup(setup)
+    oracle.rhs(u0, mesh, "ranocha", "ranocha", nthreads=1)
+    t0 = time.perf_counter()
+    n_cpu = 3
+    for _ in range(n_cpu):
+        oracle.rhs(u0, mesh, "ranocha", "ranocha", nthreads=1)
+    cpu_pid = (time.perf_counter() - t0) / n_cpu / r["dofs"]
+    return {
+        "metric": "PID (s per RHS evaluation per DOF), lower is better",
+        "value": r["mean_pid"], "std": r["std_pid"], "n_rhs": r["n_rhs"], "dofs": r["dofs"], "dt": r["dt"],
+        "workload": "3D isentropic vortex (eps=20), N=3, 8^3 elements, Ranocha/Ranocha, RK54 CFL 0.5, 90 steps",
+        "how": r["how"],
+        "cpu_oracle_pid_1_thread": cpu_pid,
+        "cpu_oracle_note": "oracle/fdg_oracle.c rhs (the reference's scalar arithmetic) on 1 host thread, 3 RHS",
+    }
+
+
+def measure_gauss(args):
+    """RHS of the Gauss-node family: 3D, N=3 on Gauss nodes,
+    32^3 curved elements (the cfg4 warp), gauss_fluxdiff, Ranocha + llf:
+    projection kernel + hybridized volume/interface kernel per RHS."""
+    import torch
+
+    from paper_2112_10517_b200 import RhsConfig, build_mesh, build_setup, gauss_operator
+    from paper_2112_10517_b200.device import gauss_mesh_for
+    from paper_2112_10517_b200.workloads import GAS, _prim2cons_torch
+
+    mesh = build_mesh((32, 32, 32), bounds=(-1.0, 1.0), amplitude=-0.1)
+    setup = build_setup(mesh, gauss_operator(3), GAS, device="cuda")
+    x = setup.coords
+    q = torch.empty(x.shape[:-1] + (5,), dtype=torch.float64, device="cuda")
+    q[..., 0] = 1.0 + 0.5 * torch.sin(torch.pi * x.sum(-1))
+    q[..., 1], q[..., 2], q[..., 3], q[..., 4] = 0.1, 0.2, 0.3, 2.0
+    u = _prim2cons_torch(q, GAS.inv_gamma_minus_one)
+    cfg = RhsConfig(volume_scheme="gauss_fluxdiff", volume_flux="ranocha", surface_flux="llf")
+    gm = gauss_mesh_for(setup, cfg.volume_scheme)
+    scheme = cfg.scheme()
+    out = gm.empty()
+    proj, nrm = gm.project(u)
+
+    def step(i):
+        gm.project(u, proj, nrm)
+        gm.rhs(u, scheme, out=out, proj=proj, nrm=nrm)
+
+    for i in range(3):
+        step(i)
+    ms, _ = _time_launches(step, 10, torch.cuda.current_stream(), None, 0, sample_clocks=False)
+    nodes = setup.n_elements * setup.n_nodes
+    return {
+        "metric": "full-RHS DOF updates/s (1/PID), fp64", "value": nodes / (ms * 1e-3), "ms_per_step": ms,
+        "nodes": nodes,
+        "workload": "Gauss nodes N=3, 32^3 curved hexes (cfg4 warp), gauss_fluxdiff Ranocha + llf, density wave",
+        "launches_per_step": 2,
+    }
+
+
 def run_ours(args, rank, world, local, dist):
     import torch
 
@@ -698,6 +767,13 @@ def run_ours(args, rank, world, local, dist):
             except Exception as err:
                 sec[kind] = {"error": repr(err)[:300]}
             torch.cuda.empty_cache()
+        if world == 1:
+            for name, fn in (("pid_vortex_3d", measure_pid), ("rhs_gauss_3d", measure_gauss)):
+                try:
+                    sec[name] = fn(args)
+                except Exception as err:
+                    sec[name] = {"error": repr(err)[:300]}
+                torch.cuda.empty_cache()
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(headline)
