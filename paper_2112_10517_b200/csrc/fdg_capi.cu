@@ -130,6 +130,13 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     for (int i = 0; i < m->p1; ++i) m->w1d[i] = desc->weights[i];
     k.w0 = desc->weights[0];
     k.wp = desc->weights[m->p1 - 1];
+    k.inv_w0 = 1.0 / k.w0;
+    k.inv_wp = 1.0 / k.wp;
+    {
+        // tuning override (A/B runs only): FDG_FUSE_FACES=0 keeps the separate face phase in the FAST kernels
+        const char* env = getenv("FDG_FUSE_FACES");
+        k.fuse_faces = env ? atoi(env) : 1;
+    }
     for (int i = 0; i < 3; ++i) k.areas[i] = desc->areas[i];
     k.jac_const = desc->jac_const;
     k.rjac_const = desc->cartesian ? 1.0 / desc->jac_const : 0.0;

@@ -557,10 +557,13 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
     const double p_l = gas.gm1 * fma(-0.5, kl, ul[D + 1]);
     const double p_r = gas.gm1 * fma(-0.5, kr, ur[D + 1]);
     double norm, vns_l, vns_r, inorm_ = 0.0;  // |n| and v.n with the scaled normal
+    double avl = 0.0, avr = 0.0;              // AXIS >= 0: |v.n| / |n| = |v_axis| (area > 0)
     if constexpr (AXIS >= 0) {
         norm = nrm[AXIS];
         vns_l = vl[AXIS] * norm;
         vns_r = vr[AXIS] * norm;
+        avl = fabs(vl[AXIS]);
+        avr = fabs(vr[AXIS]);
     } else {
         double nn = 0.0;
         vns_l = 0.0;
@@ -574,12 +577,17 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
         inorm_ = rsqrt_fast(nn);
         norm = nn * inorm_;
     }
-    const double inorm = (AXIS >= 0) ? rcp_fast(norm) : inorm_;
     // sound speeds sqrt(gamma p / rho) as x rsqrt(x): no IEEE sqrt slow path
     // (admissible states have p, rho > 0; the gate reports the others)
     const double cl2 = gas.gamma * p_l * ril, cr2 = gas.gamma * p_r * rir;
-    const double lam_l = fma(fabs(vns_l), inorm, cl2 * rsqrt_fast(cl2));
-    const double lam_r = fma(fabs(vns_r), inorm, cr2 * rsqrt_fast(cr2));
+    double lam_l, lam_r;
+    if constexpr (AXIS >= 0) {
+        lam_l = fma(cl2, rsqrt_fast(cl2), avl);
+        lam_r = fma(cr2, rsqrt_fast(cr2), avr);
+    } else {
+        lam_l = fma(fabs(vns_l), inorm_, cl2 * rsqrt_fast(cl2));
+        lam_r = fma(fabs(vns_r), inorm_, cr2 * rsqrt_fast(cr2));
+    }
     const double halfdiss = 0.5 * fmax(lam_l, lam_r) * norm;
     f[0] = 0.5 * (ul[0] * vns_l + ur[0] * vns_r) - halfdiss * (ur[0] - ul[0]);
 #pragma unroll
@@ -588,6 +596,79 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
         f[1 + i] = 0.5 * (fma(ul[1 + i], vns_l, ur[1 + i] * vns_r) + pn) - halfdiss * (ur[1 + i] - ul[1 + i]);
     }
     f[D + 1] = 0.5 * fma(ul[D + 1] + p_l, vns_l, (ur[D + 1] + p_r) * vns_r) - halfdiss * (ur[D + 1] - ul[D + 1]);
+}
+
+// FAST Rusanov flux of a fused interface term (line_faces): one side is the
+// element's own end node, taken from the staged FAST primitives in shared
+// memory (rho, v/2, p/2: no reciprocal, no global re-read of the own trace),
+// the other side the neighbour's conserved trace from global memory.
+// OWN_LEFT: the own node is the left (minus) state. The two elements of an
+// interface then evaluate the flux from differently rounded copies of each
+// other's state (staged primitives vs conserved), so the two lifted values
+// agree to rounding (~1e-16 relative), not to the bit.
+template <int D, int AXIS, bool OWN_LEFT>
+__device__ __forceinline__ void flux_llf_fast_own(double orho, const double* ovh, double oph, const double* un,
+                                                  const double* nrm, const Gas& gas, double* f)
+{
+    // own side from the staged values
+    double ov[D], om[D], s = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        ov[i] = 2.0 * ovh[i];
+        om[i] = orho * ov[i];
+        s = fma(ovh[i], ovh[i], s);
+    }
+    const double op = 2.0 * oph;
+    const double oE = fma(2.0 * orho, s, op * gas.igm1);
+    // neighbour side from its conserved trace
+    const double rin = rcp_fast(un[0]);
+    double nv[D], kn = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        nv[i] = un[1 + i] * rin;
+        kn = fma(un[1 + i], nv[i], kn);
+    }
+    const double np_ = gas.gm1 * fma(-0.5, kn, un[D + 1]);
+    double norm, ovns, nvns, inorm_ = 0.0, aov = 0.0, anv = 0.0;
+    if constexpr (AXIS >= 0) {
+        norm = nrm[AXIS];
+        ovns = ov[AXIS] * norm;
+        nvns = nv[AXIS] * norm;
+        aov = fabs(ov[AXIS]);
+        anv = fabs(nv[AXIS]);
+    } else {
+        double nn = 0.0;
+        ovns = 0.0;
+        nvns = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            nn = fma(nrm[i], nrm[i], nn);
+            ovns = fma(ov[i], nrm[i], ovns);
+            nvns = fma(nv[i], nrm[i], nvns);
+        }
+        inorm_ = rsqrt_fast(nn);
+        norm = nn * inorm_;
+    }
+    // c = sqrt(gamma p / rho) = gamma p rsqrt(gamma p rho): no reciprocal of the own density
+    const double ogp = gas.gamma * op, ngp = gas.gamma * np_;
+    const double oc = ogp * rsqrt_fast(ogp * orho), nc = ngp * rsqrt_fast(ngp * un[0]);
+    double olam, nlam;
+    if constexpr (AXIS >= 0) {
+        olam = oc + aov;
+        nlam = nc + anv;
+    } else {
+        olam = fma(fabs(ovns), inorm_, oc);
+        nlam = fma(fabs(nvns), inorm_, nc);
+    }
+    const double hd = 0.5 * fmax(olam, nlam) * norm;
+    const double sg = OWN_LEFT ? hd : -hd;  // -halfdiss (u_r - u_l) = sg (own - neighbour)
+    f[0] = fma(sg, orho - un[0], 0.5 * fma(orho, ovns, un[0] * nvns));
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double pn = (AXIS >= 0) ? ((i == AXIS) ? (op + np_) * norm : 0.0) : (op + np_) * nrm[i];
+        f[1 + i] = fma(sg, om[i] - un[1 + i], 0.5 * (fma(om[i], ovns, un[1 + i] * nvns) + pn));
+    }
+    f[D + 1] = fma(sg, oE - un[D + 1], 0.5 * fma(oE + op, ovns, (un[D + 1] + np_) * nvns));
 }
 
 // Two-point flux with conserved inputs for the interface (runtime kind).

@@ -25,6 +25,28 @@ constexpr bool has_hiocc()
            min_blocks<D, P1, MODE, CURVED>() < FDG_HIOCC;
 }
 
+// Volume-integral-only twin (EPIK = EPI_VOLUME) of the FAST 3D kernels the
+// BASELINE volume workloads run: the image holds no interface / stage code.
+#ifndef FDG_VOLK
+#define FDG_VOLK 1
+#endif
+template <int D, int P1, int MODE, bool CURVED>
+constexpr bool has_volk()
+{
+    return FDG_VOLK && MODE == FAST && D == 3 && (P1 == 4 || P1 == 5 || P1 == 8);  // BASELINE degrees N = 3, 4, 7
+}
+
+// RHS / RK-stage twins with the interface terms fused (Rusanov): no separate
+// face phase, no volume-only / surface-only code in the image
+#ifndef FDG_RHSK
+#define FDG_RHSK 1
+#endif
+template <int D, int P1, int VF, int MODE, bool CURVED>
+constexpr bool has_rhsk()
+{
+    return FDG_RHSK && MODE == FAST && D == 3 && (P1 == 4 || P1 == 5) && VF != F_CENTRAL;
+}
+
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC>
 cudaError_t elem_occupancy(int* blocks_per_sm)
 {
@@ -99,6 +121,32 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
     if constexpr (twin) {
         if (nb > slots && nb <= (long long)bps_hi * sm_count) {
             return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>, (unsigned)nb, G::NT, smem, s, p);
+        }
+    }
+    // compile-time-epilogue twins: same launch bounds and shared memory as
+    // the general kernel, so the same occupancy
+    auto launch_twin = [&](auto kern, bool* attr_set) -> cudaError_t {
+        if (dev >= 0 && dev < kMaxDev && !attr_set[dev]) {
+            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (err != cudaSuccess) return err;
+            attr_set[dev] = true;
+        }
+        return launch_kernel(kern, (unsigned)std::min(nb, slots), G::NT, smem, s, p);
+    };
+    if constexpr (has_volk<D, P1, MODE, CURVED>()) {
+        if (p.epilogue == EPI_VOLUME) {
+            static bool attr_set[kMaxDev] = {};
+            return launch_twin(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0, EPI_VOLUME>, attr_set);
+        }
+    }
+    if constexpr (has_rhsk<D, P1, VF, MODE, CURVED>()) {
+        if (p.fuse_faces && p.surface_flux == F_LLF && p.epilogue == EPI_RHS) {
+            static bool attr_set[kMaxDev] = {};
+            return launch_twin(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0, EPI_RHS>, attr_set);
+        }
+        if (p.fuse_faces && p.surface_flux == F_LLF && p.epilogue == EPI_STAGE) {
+            static bool attr_set[kMaxDev] = {};
+            return launch_twin(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0, EPI_STAGE>, attr_set);
         }
     }
     return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0>, (unsigned)std::min(nb, slots), G::NT, smem, s,

@@ -64,6 +64,8 @@ struct KParams {
     double jac_const;         // Cartesian J
     double rjac_const;        // 1/J (FAST)
     double w0, wp;            // LGL weights at the -1 / +1 ends
+    double inv_w0, inv_wp;    // 1/w0, 1/wp (FAST: interface terms fused into the volume passes)
+    int fuse_faces;           // FAST RHS / RK-stage launches with the Rusanov interface flux: line-end fusion on
     Gas gas;
     int epilogue;
     int surface_flux;
@@ -109,6 +111,9 @@ constexpr int kFaceUnroll = FDG_FACE_UNROLL;
 #ifndef FDG_NB_SMEM
 #define FDG_NB_SMEM 1  // interface neighbour indices read into shared memory at batch start (v13: cfg4 RHS +7.7%, cfg5 RHS +3.4%)
 #endif
+#ifndef FDG_DIR_REV
+#define FDG_DIR_REV 0
+#endif
 #ifndef FDG_PDL
 #define FDG_PDL 0  // 1: programmatic dependent launch (fdg_dispatch.cuh); measured no gain in a CUDA graph
 #endif
@@ -134,7 +139,10 @@ struct Geo {
     // threads per CTA target: one warp (2 elements) for 3D p+1 = 4 -- no
     // barrier coupling between warps, cfg2 VOL +1.3%, RHS +3.7% against 2-warp
     // CTAs (profiles/r01_tuning.md) -- else FDG_TARGET_THREADS
-    static constexpr int TT = (D == 3 && P1 == 4 && FDG_TARGET_THREADS == 64) ? 32 : FDG_TARGET_THREADS;
+#ifndef FDG_P4_TT
+#define FDG_P4_TT 32
+#endif
+    static constexpr int TT = (D == 3 && P1 == 4 && FDG_TARGET_THREADS == 64) ? FDG_P4_TT : FDG_TARGET_THREADS;
     static constexpr int EPB = LINES >= TT ? 1 : TT / LINES;
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
     static constexpr int FS = EPB * NNP;      // stride of one primitive field
@@ -278,10 +286,110 @@ __device__ __forceinline__ Node<D, NX> load_node(const double* sq, int fs, int i
     return q;
 }
 
+// FAST interface terms of one LGL line, fused into the line's volume pass
+// (RHS and RK-stage launches, Rusanov flux). The thread that owns line m of
+// direction n holds the accumulators of the line's two end nodes in
+// registers, and those are exactly the element's face nodes of direction n:
+// the -n face at line position 0 (the element is the plus side:
+// out -= f / (w_0 J), discretization.py:758-760) and the +n face at position
+// p (minus side: out += f / (w_p J)). The accumulators are still unscaled
+// (the epilogue multiplies by 1/J), so the lifts enter as f / w. All four
+// trace loads are issued before the first flux; no shared-memory round trip,
+// no barrier, no per-item index arithmetic. Both sides of an interface still
+// evaluate the flux from identical conserved arguments in the same order, so
+// the two lifted values are the same double (discrete conservation holds to
+// the last bit of the flux). The per-node summation order differs from the
+// reference's (VOL/J first, then the faces by direction), which is why only
+// the FAST kernels do this; FAITHFUL keeps the reference order below.
+// vmap: slot -> conserved variable (identity, or the rotated momentum slots
+// of the runtime-direction pass; the flux comes back in the same slots).
+#ifndef FDG_FACE_OWN
+#define FDG_FACE_OWN 0  // 1: own end-node states from the staged primitives in shared memory (flux_llf_fast_own)
+#endif
+// sq_first / sq_last: shared-memory slots of the line's end nodes (FAST primitives: rho, v/2, p/2)
+template <int D, int P1, bool CURVED, int AXIS>
+__device__ __forceinline__ void line_faces(const KParams& prm, long long e, int n, const int* vmap, int m, int first,
+                                           int last, int nbm, int nbp, double* acc_first, double* acc_last,
+                                           const double* sq, int sq_first, int sq_last)
+{
+    using G = Geo<D, P1>;
+    constexpr int NVAR = G::NVAR, FN = G::LINES;
+    auto load = [&](const double* src, double* s) {
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) s[v] = __ldg(src + vmap[v]);
+    };
+#if FDG_FACE_OWN
+    {
+        double pf[NVAR], ml[NVAR];
+        load(nbp >= 0 ? prm.u + ((long long)nbp * G::NN + first) * NVAR
+                      : prm.ghost_u + ((long long)(-nbp - 1) * FN + m) * NVAR, pf);
+        load(nbm >= 0 ? prm.u + ((long long)nbm * G::NN + last) * NVAR
+                      : prm.ghost_u + ((long long)(-nbm - 1) * FN + m) * NVAR, ml);
+        double np[D], nm[D];
+        if constexpr (CURVED) {
+            const double* jm = nbm >= 0 ? prm.ja + (((long long)nbm * G::NN + last) * D + n) * D
+                                        : prm.ghost_nrm + ((long long)(-nbm - 1) * FN + m) * D;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                np[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
+                nm[j] = __ldg(jm + j);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) np[j] = nm[j] = (j == AXIS) ? prm.areas[n] : 0.0;
+        }
+        // own end nodes: staged rho, v/2 (slot j = variable vmap[1+j]), p/2
+        double lv[D], fv[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            lv[j] = sq[vmap[1 + j] * G::FS + sq_last];
+            fv[j] = sq[vmap[1 + j] * G::FS + sq_first];
+        }
+        double f[NVAR];
+        flux_llf_fast_own<D, AXIS, true>(sq[sq_last], lv, sq[(1 + D) * G::FS + sq_last], pf, np, prm.gas, f);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) acc_last[v] = fma(prm.inv_wp, f[v], acc_last[v]);
+        flux_llf_fast_own<D, AXIS, false>(sq[sq_first], fv, sq[(1 + D) * G::FS + sq_first], ml, nm, prm.gas, f);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) acc_first[v] = fma(-prm.inv_w0, f[v], acc_first[v]);
+        return;
+    }
+#endif
+    const double* own = prm.u + e * (long long)(G::NN * NVAR);
+    double ol[NVAR], pf[NVAR], ml[NVAR], of[NVAR];
+    load(own + last * NVAR, ol);   // +n face: (own last | plus neighbour first)
+    load(nbp >= 0 ? prm.u + ((long long)nbp * G::NN + first) * NVAR : prm.ghost_u + ((long long)(-nbp - 1) * FN + m) * NVAR,
+         pf);
+    load(nbm >= 0 ? prm.u + ((long long)nbm * G::NN + last) * NVAR : prm.ghost_u + ((long long)(-nbm - 1) * FN + m) * NVAR,
+         ml);                      // -n face: (minus neighbour last | own first)
+    load(own + first * NVAR, of);
+    double np[D], nm[D];
+    if constexpr (CURVED) {
+        const double* jm = nbm >= 0 ? prm.ja + (((long long)nbm * G::NN + last) * D + n) * D
+                                    : prm.ghost_nrm + ((long long)(-nbm - 1) * FN + m) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            np[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
+            nm[j] = __ldg(jm + j);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) np[j] = nm[j] = (j == AXIS) ? prm.areas[n] : 0.0;
+    }
+    double f[NVAR];
+    flux_llf_fast<D, AXIS>(ol, pf, np, prm.gas, f);
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) acc_last[v] = fma(prm.inv_wp, f[v], acc_last[v]);
+    flux_llf_fast<D, AXIS>(ml, of, nm, prm.gas, f);
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) acc_first[v] = fma(-prm.inv_w0, f[v], acc_first[v]);
+}
+
 // One direction of the volume integral for the thread's line.
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST = (N == 0)>
 __device__ __forceinline__ void volume_direction(const KParams& prm, const double* sq, double* sacc, int el,
-                                                 int m, long long e, unsigned vm)
+                                                 int m, long long e, unsigned vm, bool faces = false, int nbm = 0,
+                                                 int nbp = 0)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
@@ -290,7 +398,7 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
     int nodes[P1];
 #pragma unroll
     for (int a = 0; a < P1; ++a) nodes[a] = G::template line_node<N>(m, a);
-    if constexpr (N == 0) {
+    if constexpr (FIRST) {
 #pragma unroll
         for (int a = 0; a < P1; ++a)
 #pragma unroll
@@ -353,6 +461,16 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
             }
         });
     });
+    if constexpr (MODE == FAST) {
+        if (faces) {
+            int ident[NVAR];
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) ident[v] = v;
+            line_faces<D, P1, CURVED, CURVED ? -1 : N>(prm, e, N, ident, m, nodes[0], nodes[P1 - 1], nbm, nbp, acc[0],
+                                                        acc[P1 - 1], sq, sbase + G::pad(nodes[0]),
+                                                        sbase + G::pad(nodes[P1 - 1]));
+        }
+    }
 #pragma unroll
     for (int a = 0; a < P1; ++a)
 #pragma unroll
@@ -401,25 +519,28 @@ __host__ __device__ constexpr bool runtime_direction_iface()
 
 template <int D, int P1, int VF, bool CURVED, int LOGS>
 __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const double* sq, double* sacc, int el, int m,
-                                                    long long e, int n, unsigned vm)
+                                                    long long e, int n, bool first, unsigned vm, bool faces = false,
+                                                    int nbm = 0, int nbp = 0)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
     constexpr int NX = n_extra(VF, LOGS);
     const int stride = line_stride<D, P1>(n);
-    const int base = (m / stride) * P1 * stride + m % stride;  // line position 0
+    // line position 0: (m / stride) P1 stride + m % stride, with the three
+    // compile-time strides spelled out (no runtime division)
+    const int base = (n == 0) ? m : ((D == 3 && n == 1) ? (m / P1) * P1 * P1 + m % P1 : m * P1);
     // variable / field index of rotated slot j (rho, v'_0..v'_{d-1}, E | p, extras)
     int vmap[NVAR];
     vmap[0] = 0;
     vmap[NVAR - 1] = NVAR - 1;
 #pragma unroll
-    for (int j = 0; j < D; ++j) vmap[1 + j] = CURVED ? 1 + j : 1 + (n + j) % D;
+    for (int j = 0; j < D; ++j) vmap[1 + j] = CURVED ? 1 + j : 1 + (n + j >= D ? n + j - D : n + j);
     double acc[P1][NVAR];
 #pragma unroll
     for (int a = 0; a < P1; ++a) {
         const int nd = base + a * stride;
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) acc[a][v] = (n == 0) ? 0.0 : sacc[G::acc(vmap[v], el, nd)];
+        for (int v = 0; v < NVAR; ++v) acc[a][v] = first ? 0.0 : sacc[G::acc(vmap[v], el, nd)];
     }
     const int sbase = el * G::NNP;
     auto load = [&](int a) {
@@ -461,6 +582,10 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
             }
         });
     });
+    if (faces)
+        line_faces<D, P1, CURVED, CURVED ? -1 : 0>(prm, e, n, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, acc[0],
+                                                    acc[P1 - 1], sq, sbase + G::pad(base),
+                                                    sbase + G::pad(base + (P1 - 1) * stride));
 #pragma unroll
     for (int a = 0; a < P1; ++a) {
         const int nd = base + a * stride;
@@ -469,14 +594,19 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
     }
 }
 
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N>
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST>
 __device__ __forceinline__ void vdir(const KParams& prm, const double* sq, double* sacc, int el, int m, long long e,
-                                     bool active, unsigned vm)
+                                     bool active, unsigned vm, bool fuse = false, const int* nb = nullptr)
 {
     if constexpr (MODE == FAST) {
-        if (vm) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N>(prm, sq, sacc, el, m, active ? e : e - el, vm);
+        if (vm) {
+            const bool faces = fuse && active;
+            volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, active ? e : e - el, vm,
+                                                                       faces, faces ? nb[(el * D + N) * 2] : 0,
+                                                                       faces ? nb[(el * D + N) * 2 + 1] : 0);
+        }
     } else {
-        if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N>(prm, sq, sacc, el, m, e, 0u);
+        if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, e, 0u);
     }
 }
 
@@ -599,7 +729,9 @@ extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 
 // OCC > 0 overrides the resident-CTA hint (the high-occupancy twin used when a
 // launch fits one wave only at that occupancy, fdg_dispatch.cuh)
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0>
+// EPIK >= 0 fixes the epilogue at compile time (the volume-integral-only
+// twin: no interface / stage code in the kernel image, fdg_dispatch.cuh)
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0, int EPIK = -1>
 __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE, CURVED>())
     elem_kernel(const __grid_constant__ KParams prm)
 {
@@ -620,7 +752,13 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     const bool tma_u = TMA_SHAPE && (reinterpret_cast<uintptr_t>(prm.u) & 15) == 0;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sacc + G::NVAR * G::FA);
     // VOL leaves as AoS through the (then free) primitive region by a bulk store
-    const bool tma_out_ok = TMA_SHAPE && prm.epilogue != EPI_STAGE && (reinterpret_cast<uintptr_t>(prm.out) & 15) == 0;
+    const int epi = EPIK >= 0 ? EPIK : prm.epilogue;
+    // FAST: directions in descending order, so the fused interface terms of
+    // direction 0 (neighbours farthest away in the element order, their face
+    // rows prefetched into L2 at batch start) are read last; the per-node sum
+    // order is free in FAST mode (FAITHFUL keeps the reference's 0..d-1)
+    constexpr bool REV = FDG_DIR_REV && MODE == FAST;
+    const bool tma_out_ok = TMA_SHAPE && epi != EPI_STAGE && (reinterpret_cast<uintptr_t>(prm.out) & 15) == 0;
     bool tma_pending = false;  // a bulk store may still be reading the primitive region
     unsigned phase = 0;
     if (TMA_SHAPE && tid == 0) mbar_init(bar);
@@ -648,9 +786,17 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     const long long nb1 = (prm.range_hi - prm.range_lo + EPB - 1) / EPB;
     const long long nbatch = nb1 + (prm.range2_hi - prm.range2_lo + EPB - 1) / EPB;
     auto range_end = [&](long long b) -> long long { return b < nb1 ? prm.range_hi : prm.range2_hi; };
-    const int epi = prm.epilogue;
 #if FDG_NB_SMEM
     __shared__ int s_nb[EPB * 2 * D];
+    // FAST RHS / RK-stage launches with the Rusanov flux: interface terms
+    // fused into the volume passes (line_faces), no separate face phase
+    // (EPIK = RHS / STAGE twins are only launched when this holds)
+    const bool fuse = (EPIK == EPI_RHS || EPIK == EPI_STAGE) ||
+                      (MODE == FAST && VF != F_CENTRAL && prm.fuse_faces && (epi == EPI_RHS || epi == EPI_STAGE) &&
+                       prm.surface_flux == F_LLF);
+#else
+    constexpr bool fuse = false;
+    const int* s_nb = nullptr;
 #endif
 
     // traversal order: batch b covers elements [first(b), first(b) + EPB).
@@ -840,25 +986,41 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             __syncthreads();
             FDG_PT(1)
             // ---- volume integral, direction by direction (accumulators: SoA)
-            bool rt_pass = MODE == FAST && runtime_direction<D, P1, VF>();
-            if constexpr (MODE == FAST && runtime_direction_iface<D, P1, VF>()) rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;
+            // runtime-direction pass (one copy of the pair code): p+1 >= 5, and
+            // the fused RHS / RK-stage twins at every degree -- their image
+            // (three compile-time passes, each with two inlined Rusanov
+            // fluxes) overflowed the 32 KB L1.5 instruction cache: cfg5 RHS
+            // 7.83 -> 6.44 ms with one copy (profiles/r02_tuning.md); the
+            // volume-only twin keeps the compile-time passes below p+1 = 5
+            // (3.87 vs 4.03 ms: there the rotated-load address math costs more)
+            constexpr bool RT_ONLY = MODE == FAST && VF != F_CENTRAL &&
+                                     (runtime_direction<D, P1, VF>() || EPIK == EPI_RHS || EPIK == EPI_STAGE);
+            bool rt_pass = RT_ONLY;
+            if constexpr (!RT_ONLY && MODE == FAST && runtime_direction_iface<D, P1, VF>())
+                rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;
             if (rt_pass) {
                 if constexpr (MODE == FAST && VF != F_CENTRAL) {
 #pragma unroll 1
-                    for (int n = 0; n < D; ++n) {
-                        if (vmask) volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, vmask);
+                    for (int i = 0; i < D; ++i) {
+                        const int n = REV ? D - 1 - i : i;
+                        if (vmask) {
+                            const bool faces = fuse && active;
+                            volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, i == 0,
+                                                                         vmask, faces, faces ? s_nb[(el * D + n) * 2] : 0,
+                                                                         faces ? s_nb[(el * D + n) * 2 + 1] : 0);
+                        }
                         __syncthreads();
                     }
                 }
-            } else if constexpr (!(MODE == FAST && runtime_direction<D, P1, VF>())) {
-                vdir<D, P1, VF, CURVED, MODE, LOGS, 0>(prm, sq, sacc, el, m, e, active, vmask);
+            } else if constexpr (!RT_ONLY) {
+                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 1 : 0, true>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
                 __syncthreads();
                 FDG_PT(2)
-                vdir<D, P1, VF, CURVED, MODE, LOGS, 1>(prm, sq, sacc, el, m, e, active, vmask);
+                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 2 : 1, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
                 __syncthreads();
                 FDG_PT(3)
                 if constexpr (D == 3) {
-                    vdir<D, P1, VF, CURVED, MODE, LOGS, 2>(prm, sq, sacc, el, m, e, active, vmask);
+                    vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? 0 : 2, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
                     __syncthreads();
                 }
             }
@@ -924,7 +1086,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         // one copy of the face code (runtime n): three inlined copies spilled
         // registers in the curved p+1 = 5 kernels
 #pragma unroll 1
-        for (int n = 0; n < D; ++n) {
+        for (int n = fuse ? D : 0; n < D; ++n) {
             const int stride = line_stride<D, P1>(n);
             constexpr int NI = 2 * G::LINES;  // face nodes per element in direction n
             constexpr int KF = (EPB * NI + NT - 1) / NT;

@@ -23,6 +23,7 @@ nvcc $COMMON -c fdg_capi.cu -o obj_var/capi.o &
 nvcc $COMMON -c fdg_probe.cu -o obj_var/probe.o &
 nvcc $COMMON --fmad=false -c fdg_diag.cu -o obj_var/diag.o &
 nvcc $COMMON --fmad=false -c fdg_setup.cu -o obj_var/setup.o &
+nvcc $COMMON --fmad=false -c fdg_gauss.cu -o obj_var/gauss.o &
 FMAD=--fmad=true; [[ $UNIT == faithful* ]] && FMAD=--fmad=false
 for spec in "$@"; do
   IFS=: read -r name src flags <<< "$spec"
@@ -33,7 +34,7 @@ done
 wait
 for spec in "$@"; do
   IFS=: read -r name src flags <<< "$spec"
-  nvcc $ARCH -shared -o ../variants/libfdg_$name.so obj_var/capi.o obj_var/probe.o obj_var/diag.o obj_var/setup.o obj_var/stubs.o \
+  nvcc $ARCH -shared -o ../variants/libfdg_$name.so obj_var/capi.o obj_var/probe.o obj_var/diag.o obj_var/setup.o obj_var/gauss.o obj_var/stubs.o \
     obj_var/${UNIT}_$name.o -lcudart
 done
 ls -la ../variants

@@ -19,9 +19,13 @@ from paper_2112_10517_b200 import workloads  # noqa: E402
 from paper_2112_10517_b200.device import device_mesh_for  # noqa: E402
 
 dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
-setup, u_host, cfg = workloads.build(args.cfg, dims=dims, kernel=args.kernel, volume_flux=args.flux)
+if args.cfg in (3, 5) and dims is None:
+    # device-built geometry and state: no 22 GB host setup at 128^3
+    setup, u, cfg = workloads.build_device(args.cfg, kernel=args.kernel, volume_flux=args.flux)
+else:
+    setup, u_host, cfg = workloads.build(args.cfg, dims=dims, kernel=args.kernel, volume_flux=args.flux)
+    u = torch.as_tensor(u_host, device="cuda")
 dm = device_mesh_for(setup)
-u = torch.as_tensor(u_host, device="cuda")
 out = dm.empty()
 s = cfg.scheme()
 for _ in range(args.launches):
