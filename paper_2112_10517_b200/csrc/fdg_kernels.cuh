@@ -817,7 +817,10 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     // resident late (SMs held by concurrent work: the halo exchange's NCCL
     // kernels next to an interior launch) then takes fewer batches instead of
     // stretching the kernel's tail by its delay
-    constexpr long long kClaim = 4;
+#ifndef FDG_CLAIM_CHUNK
+#define FDG_CLAIM_CHUNK 4
+#endif
+    constexpr long long kClaim = FDG_CLAIM_CHUNK;
     const bool dyn = prm.claim != nullptr;
     __shared__ long long s_claim;
     long long batch = blockIdx.x, chunk_end = 0;
