@@ -573,8 +573,8 @@ def _e2e_volume(args, slab, u_dev, config, local, dist, nodes_total, world):
         "numpy_path": {
             "value": nodes_total / (np_ms_max * 1e-3),
             "ms_per_step": np_ms_max,
-            "how": "mesh_fluxdiff_volume(numpy array) -> new numpy array (host memcpy into pinned staging, "
-                   "the same chunked pipeline, host memcpy out); wall clock, best of 2",
+            "how": "mesh_fluxdiff_volume(numpy array) -> new numpy array (multi-threaded host copy into pinned staging, "
+                   "the same chunked pipeline, multi-threaded copy out); wall clock, best of 2",
         },
     }
 

@@ -172,11 +172,14 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         delete m;
         return cuda_fail(err, "cudaMalloc(claim counter)");
     }
-    // interface epilogues (RHS, RK stage, surface) claim batches dynamically;
-    // the volume integral keeps the static order (FDG_DYN_CLAIM=0|1|2 tunes: off | interface | all)
+    // launches deeper than one batch per CTA claim batches dynamically
+    // (FDG_DYN_CLAIM=0|1|2 tunes: off | interface epilogues only | all)
     {
         const char* env = getenv("FDG_DYN_CLAIM");
-        m->dyn_claim = env ? atoi(env) : 1;
+        m->dyn_claim = env ? atoi(env) : 2;
+        // (round 2: the volume integral claims dynamically too: cfg5 VOL 3.87 -> 3.57 ms)
+        k.claim_chunk_max = 1;
+        k.claim_chunk = 1;
         // runtime-direction volume pass in the p+1 <= 4 interface kernels:
         // measured slower (cfg5 RHS 9.42 vs 8.92 ms with dynamic claiming,
         // profiles/r02_ab_rt_dc.txt), off by default
@@ -187,7 +190,11 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         long long nn = 1;
         for (int i = 0; i < m->d; ++i) nn *= m->p1;
         const double state_bytes = (double)m->n_elem * (double)nn * (m->d + 2) * 8.0;
-        k.face_prefetch = state_bytes > 8.0 * 126.0 * 1024 * 1024;  // >> the 126 MB L2
+        // round 2: off by default -- with the interface terms fused into the
+        // volume passes it measured 1.2% slower (profiles/r02_tuning.md); the
+        // size gate below is what FDG_FACE_PREFETCH=1 meant before
+        (void)state_bytes;
+        k.face_prefetch = 0;
         // tuning override (A/B runs only): FDG_FACE_PREFETCH=0|1
         if (const char* env = getenv("FDG_FACE_PREFETCH")) k.face_prefetch = atoi(env) != 0;
     }

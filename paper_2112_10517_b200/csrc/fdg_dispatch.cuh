@@ -89,8 +89,9 @@ cudaError_t launch_kernel(Kern kern, unsigned grid, unsigned block, size_t smem,
 }
 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS>
-cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
+cudaError_t launch_elem(const KParams& p_in, cudaStream_t s, int sm_count)
 {
+    KParams p = p_in;
     using G = Geo<D, P1>;
     constexpr size_t smem = (size_t)smem_doubles<D, P1, VF, LOGS>() * sizeof(double);
     constexpr bool twin = has_hiocc<D, P1, MODE, CURVED>();
@@ -118,8 +119,12 @@ cudaError_t launch_elem(const KParams& p, cudaStream_t s, int sm_count)
     const long long nb = (p.range_hi - p.range_lo + G::EPB - 1) / G::EPB + (p.range2_hi - p.range2_lo + G::EPB - 1) / G::EPB;
     if (nb <= 0) return cudaSuccess;
     const long long slots = (long long)bps * std::max(1, sm_count - std::max(0, p.reserve_sms));
+    // dynamic claiming (one batch per claim, fdg_kernels.cuh); a launch of at
+    // most one batch per CTA keeps the static assignment
+    if (p.claim && nb <= slots) p.claim = nullptr;
     if constexpr (twin) {
         if (nb > slots && nb <= (long long)bps_hi * sm_count) {
+            p.claim = nullptr;  // one batch per CTA
             return launch_kernel(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC>, (unsigned)nb, G::NT, smem, s, p);
         }
     }

@@ -55,6 +55,8 @@ struct KParams {
     long long range2_lo;      // optional second range [range2_lo, range2_hi) in the same launch
     long long range2_hi;      //   (both boundary planes of a slab in one launch); empty by default
     unsigned long long* claim; // dynamic batch claiming: [0] next batch, [1] CTAs done (null: static grid-stride)
+    int claim_chunk;          // (unused since claims are per batch, one ahead; kept for the parameter-block layout)
+    int claim_chunk_max;
     int rt_iface;             // interface epilogues below FDG_RT_DIR_MIN_P1 take the runtime-direction pass
     int reserve_sms;          // launch only on sm_count - reserve_sms SMs' worth of CTAs (room for concurrent
                               // halo kernels: a full-occupancy grid holds every register of every SM)
@@ -303,8 +305,65 @@ __device__ __forceinline__ Node<D, NX> load_node(const double* sq, int fs, int i
 // the FAST kernels do this; FAITHFUL keeps the reference order below.
 // vmap: slot -> conserved variable (identity, or the rotated momentum slots
 // of the runtime-direction pass; the flux comes back in the same slots).
+// the neighbours' facing traces of line m (plus neighbour's first node,
+// minus neighbour's last node), slot v = conserved variable vmap[v]
+template <int D, int P1>
+__device__ __forceinline__ void line_faces_load(const KParams& prm, const int* vmap, int m, int first, int last, int nbm,
+                                                int nbp, double* pf, double* ml)
+{
+    using G = Geo<D, P1>;
+    constexpr int NVAR = G::NVAR, FN = G::LINES;
+    const double* sp = nbp >= 0 ? prm.u + ((long long)nbp * G::NN + first) * NVAR
+                                : prm.ghost_u + ((long long)(-nbp - 1) * FN + m) * NVAR;
+    const double* sm = nbm >= 0 ? prm.u + ((long long)nbm * G::NN + last) * NVAR
+                                : prm.ghost_u + ((long long)(-nbm - 1) * FN + m) * NVAR;
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+        pf[v] = __ldg(sp + vmap[v]);
+        ml[v] = __ldg(sm + vmap[v]);
+    }
+}
+
+// the two Rusanov fluxes of the line's end nodes (own side from the staged
+// FAST primitives, flux_llf_fast_own) lifted as f / w into the accumulators
+template <int D, int P1, bool CURVED, int AXIS>
+__device__ __forceinline__ void line_faces_apply(const KParams& prm, long long e, int n, const int* vmap, int m, int last,
+                                                 int nbm, const double* pf, const double* ml, double* acc_first,
+                                                 double* acc_last, const double* sq, int sq_first, int sq_last)
+{
+    using G = Geo<D, P1>;
+    constexpr int NVAR = G::NVAR, FN = G::LINES;
+    double np[D], nm[D];
+    if constexpr (CURVED) {
+        const double* jm = nbm >= 0 ? prm.ja + (((long long)nbm * G::NN + last) * D + n) * D
+                                    : prm.ghost_nrm + ((long long)(-nbm - 1) * FN + m) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            np[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
+            nm[j] = __ldg(jm + j);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) np[j] = nm[j] = (j == AXIS) ? prm.areas[n] : 0.0;
+    }
+    // own end nodes: staged rho, v/2 (slot j = variable vmap[1+j]), p/2
+    double lv[D], fv[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        lv[j] = sq[vmap[1 + j] * G::FS + sq_last];
+        fv[j] = sq[vmap[1 + j] * G::FS + sq_first];
+    }
+    double f[NVAR];
+    flux_llf_fast_own<D, AXIS, true>(sq[sq_last], lv, sq[(1 + D) * G::FS + sq_last], pf, np, prm.gas, f);
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) acc_last[v] = fma(prm.inv_wp, f[v], acc_last[v]);
+    flux_llf_fast_own<D, AXIS, false>(sq[sq_first], fv, sq[(1 + D) * G::FS + sq_first], ml, nm, prm.gas, f);
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) acc_first[v] = fma(-prm.inv_w0, f[v], acc_first[v]);
+}
+
 #ifndef FDG_FACE_OWN
-#define FDG_FACE_OWN 0  // 1: own end-node states from the staged primitives in shared memory (flux_llf_fast_own)
+#define FDG_FACE_OWN 1  // own end-node states from the staged primitives in shared memory (flux_llf_fast_own): cfg5 RHS 6.35 -> 5.52 ms
 #endif
 // sq_first / sq_last: shared-memory slots of the line's end nodes (FAST primitives: rho, v/2, p/2)
 template <int D, int P1, bool CURVED, int AXIS>
@@ -321,37 +380,9 @@ __device__ __forceinline__ void line_faces(const KParams& prm, long long e, int 
 #if FDG_FACE_OWN
     {
         double pf[NVAR], ml[NVAR];
-        load(nbp >= 0 ? prm.u + ((long long)nbp * G::NN + first) * NVAR
-                      : prm.ghost_u + ((long long)(-nbp - 1) * FN + m) * NVAR, pf);
-        load(nbm >= 0 ? prm.u + ((long long)nbm * G::NN + last) * NVAR
-                      : prm.ghost_u + ((long long)(-nbm - 1) * FN + m) * NVAR, ml);
-        double np[D], nm[D];
-        if constexpr (CURVED) {
-            const double* jm = nbm >= 0 ? prm.ja + (((long long)nbm * G::NN + last) * D + n) * D
-                                        : prm.ghost_nrm + ((long long)(-nbm - 1) * FN + m) * D;
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                np[j] = __ldg(prm.ja + ((e * G::NN + last) * D + n) * D + j);
-                nm[j] = __ldg(jm + j);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < D; ++j) np[j] = nm[j] = (j == AXIS) ? prm.areas[n] : 0.0;
-        }
-        // own end nodes: staged rho, v/2 (slot j = variable vmap[1+j]), p/2
-        double lv[D], fv[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            lv[j] = sq[vmap[1 + j] * G::FS + sq_last];
-            fv[j] = sq[vmap[1 + j] * G::FS + sq_first];
-        }
-        double f[NVAR];
-        flux_llf_fast_own<D, AXIS, true>(sq[sq_last], lv, sq[(1 + D) * G::FS + sq_last], pf, np, prm.gas, f);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) acc_last[v] = fma(prm.inv_wp, f[v], acc_last[v]);
-        flux_llf_fast_own<D, AXIS, false>(sq[sq_first], fv, sq[(1 + D) * G::FS + sq_first], ml, nm, prm.gas, f);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) acc_first[v] = fma(-prm.inv_w0, f[v], acc_first[v]);
+        line_faces_load<D, P1>(prm, vmap, m, first, last, nbm, nbp, pf, ml);
+        line_faces_apply<D, P1, CURVED, AXIS>(prm, e, n, vmap, m, last, nbm, pf, ml, acc_first, acc_last, sq, sq_first,
+                                               sq_last);
         return;
     }
 #endif
@@ -556,11 +587,26 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
         return q;
     };
     const double* w = prm.wts[n];
+    // FDG_FACE_EARLY: where the neighbour-trace loads of the fused interface
+    // terms are issued -- 0: after the pair loop (with the fluxes), 1: before
+    // the last pair (one flux evaluation hides the L2 latency), 2: before
+    // the pair loop
+#ifndef FDG_FACE_EARLY
+#define FDG_FACE_EARLY 0
+#endif
+    constexpr bool EARLY = FDG_FACE_OWN && FDG_FACE_EARLY > 0;
+    [[maybe_unused]] double pf[NVAR], ml[NVAR];
+    if constexpr (EARLY && FDG_FACE_EARLY == 2) {
+        if (faces) line_faces_load<D, P1>(prm, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, pf, ml);
+    }
     sfor<0, P1>([&](auto A) {
         constexpr int a = decltype(A)::value;
         const Node<D, NX> qa = load(a);
         sfor<a + 1, P1>([&](auto B) {
             constexpr int b = decltype(B)::value;
+            if constexpr (EARLY && FDG_FACE_EARLY == 1 && a == P1 - 2 && b == P1 - 1) {
+                if (faces) line_faces_load<D, P1>(prm, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, pf, ml);
+            }
             const Node<D, NX> qb = load(b);
             const double wa = w[a * P1 + b];
             const double wb = w[b * P1 + a];
@@ -582,10 +628,16 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
             }
         });
     });
-    if (faces)
-        line_faces<D, P1, CURVED, CURVED ? -1 : 0>(prm, e, n, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, acc[0],
-                                                    acc[P1 - 1], sq, sbase + G::pad(base),
-                                                    sbase + G::pad(base + (P1 - 1) * stride));
+    if (faces) {
+        if constexpr (EARLY)
+            line_faces_apply<D, P1, CURVED, CURVED ? -1 : 0>(prm, e, n, vmap, m, base + (P1 - 1) * stride, nbm, pf, ml,
+                                                              acc[0], acc[P1 - 1], sq, sbase + G::pad(base),
+                                                              sbase + G::pad(base + (P1 - 1) * stride));
+        else
+            line_faces<D, P1, CURVED, CURVED ? -1 : 0>(prm, e, n, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp,
+                                                        acc[0], acc[P1 - 1], sq, sbase + G::pad(base),
+                                                        sbase + G::pad(base + (P1 - 1) * stride));
+    }
 #pragma unroll
     for (int a = 0; a < P1; ++a) {
         const int nd = base + a * stride;
@@ -812,37 +864,42 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
     };
 
-    // batch assignment: static grid-stride, or dynamic claiming in chunks of
-    // kClaim batches from a per-mesh counter (prm.claim) -- a CTA that becomes
-    // resident late (SMs held by concurrent work: the halo exchange's NCCL
-    // kernels next to an interior launch) then takes fewer batches instead of
-    // stretching the kernel's tail by its delay
-#ifndef FDG_CLAIM_CHUNK
-#define FDG_CLAIM_CHUNK 4
-#endif
-    constexpr long long kClaim = FDG_CLAIM_CHUNK;
+    // batch assignment: static grid-stride, or dynamic claiming, one batch at
+    // a time, from a per-mesh counter (prm.claim): no tail imbalance (r02_v2
+    // capture: 3.36 of 4 warps per scheduler active on average with the static
+    // order, 3.98 with claiming; cfg5 VOL 3.87 -> 3.57 ms), and a CTA that
+    // becomes resident late (SMs held by the halo exchange's NCCL kernels next
+    // to an interior launch) takes fewer batches instead of stretching the
+    // tail. Claims run ONE BATCH AHEAD: while batch i is processed the CTA
+    // already knows batch i+1 (so the L2 prefetch below is exact) and thread
+    // 0's atomic for batch i+2 is in flight, its result parked in a register
+    // until the end of the iteration (no exposed atomic latency).
     const bool dyn = prm.claim != nullptr;
-    __shared__ long long s_claim;
-    long long batch = blockIdx.x, chunk_end = 0;
+    __shared__ long long s_claim[2];
+    long long batch = blockIdx.x, next = 0;
+    [[maybe_unused]] long long pending = 0;
     if (dyn) {
-        if (tid == 0) s_claim = (long long)atomicAdd(prm.claim, (unsigned long long)kClaim);
+        if (tid == 0) {
+            s_claim[0] = (long long)atomicAdd(prm.claim, 1ull);
+            s_claim[1] = (long long)atomicAdd(prm.claim, 1ull);
+        }
         __syncthreads();
-        batch = s_claim;
-        chunk_end = batch + kClaim;
+        batch = s_claim[0];
+        next = s_claim[1];
+        __syncthreads();
     }
     auto advance = [&]() {
         if (!dyn) {
             batch += gridDim.x;
             return;
         }
-        if (++batch < chunk_end) return;
-        __syncthreads();
-        if (tid == 0) s_claim = (long long)atomicAdd(prm.claim, (unsigned long long)kClaim);
-        __syncthreads();
-        batch = s_claim;
-        chunk_end = batch + kClaim;
+        if (tid == 0) s_claim[0] = pending;
+        __syncthreads();  // (every iteration has a block barrier between this read and the next write)
+        batch = next;
+        next = s_claim[0];
     };
     for (; batch < nbatch; advance()) {
+        if (dyn && tid == 0) pending = (long long)atomicAdd(prm.claim, 1ull);
         const long long e0 = first(batch);
         const int ne = (int)min((long long)EPB, range_end(batch) - e0);
         const long long base = e0 * NN * NVAR;
@@ -859,8 +916,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         // curved meshes) while this one computes: the next staging copy then
         // waits on L2, not HBM, latency
         {
-            const long long nb = !dyn ? batch + gridDim.x
-                                 : (batch + 1 < chunk_end ? batch + 1 : batch + (long long)gridDim.x * kClaim);
+            const long long nb = !dyn ? batch + gridDim.x : next;
             if (nb < nbatch) {
                 const long long f2 = first(nb);
                 const long long ne2 = min((long long)EPB, range_end(nb) - f2);

@@ -151,17 +151,25 @@ class DeviceMesh:
         """Opt-in tile-by-tile traversal (fdg_mesh_set_traversal), env
         FDG_TILE="tx,ty": rows of dims[2] elements visited in tiles of
         tx x ty rows so the +-x / +-y interface neighbours are staged by the
-        same wave. Off by default: on cfg5 128^3 RHS it measured 1-3% slower
-        than the natural order with the face-row prefetch
-        (profiles/r01_tuning.md, v13)."""
+        same wave (FDG_TILE=0: natural order)."""
         mesh = getattr(setup, "mesh", None)
         dims = tuple(getattr(mesh, "dims", ()))
         env = os.environ.get("FDG_TILE")
-        if self.d != 3 or len(dims) != 3 or env in (None, "", "0"):
+        if self.d != 3 or len(dims) != 3 or env in ("", "0"):
             return
-        tx, ty = (int(v) for v in env.split(","))
         _, n1, n2 = dims
         n0 = self.n_elem // (n1 * n2)  # planes held here (slab partitions split direction 0)
+        if env is None:
+            # default: 8 x 8 rows per tile when the state is much larger than
+            # L2 (the +-x neighbours' traces then come from L2 instead of
+            # DRAM: cfg5 RHS 6.35 -> 6.25 ms, profiles/r02_tuning.md);
+            # L2-sized meshes keep the natural order (cfg4 48^3: 1% slower tiled)
+            state_bytes = self.n_elem * self.nn * self.nvar * 8
+            if state_bytes <= 8 * 126 * 2**20 or n0 % 8 or n1 % 8:
+                return
+            tx, ty = 8, 8
+        else:
+            tx, ty = (int(v) for v in env.split(","))
         if n0 * n1 * n2 != self.n_elem or n0 % tx or n1 % ty:
             return
         r = np.arange(n0 * n1).reshape(n0 // tx, tx, n1 // ty, ty).transpose(0, 2, 1, 3).ravel()
