@@ -126,7 +126,10 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
     // curved ones (discretization.py:318-320)
     for (int n = 0; n < 3; ++n)
         for (int i = 0; i < m->p1 * m->p1; ++i)
+        {
             k.wts[n][i] = desc->cartesian ? desc->dsplit[i] * desc->areas[n] : desc->dsplit[i];
+            k.wtsE[n][i] = 2.0 * k.wts[n][i];
+        }
     for (int i = 0; i < m->p1; ++i) m->w1d[i] = desc->weights[i];
     k.w0 = desc->weights[0];
     k.wp = desc->weights[m->p1 - 1];

@@ -207,8 +207,13 @@ __device__ __forceinline__ int gate_fast(const double* u, double p_fast, double 
 {
     // 1: admissible, 0: not, -1: |p| too close to 0 for the FAST pressure's
     // sign to be trusted -> the caller re-runs gate_ok (reference formula)
+    // rho positive, normal and finite in one unsigned compare on its high
+    // word (a positive subnormal density goes to the reference test); an
+    // infinite or NaN p_fast fails the magnitude comparison's finite side
     const double rho = u[0];
-    const bool clear = (rho > 0.0) && isfinite(rho) && isfinite(p_fast) && fabs(p_fast) > 1e-10 * gm1 * fabs(u[D + 1]);
+    const bool rho_ok = (unsigned)(__double2hiint(rho) - 0x00100000) < 0x7fe00000u;
+    const double ap = fabs(p_fast);
+    const bool clear = rho_ok && ap <= 1.7976931348623157e308 && ap > 1e-10 * gm1 * fabs(u[D + 1]);
     return clear ? (p_fast > 0.0 ? 1 : 0) : -1;
 }
 
@@ -447,11 +452,11 @@ struct Gas {
 };
 
 // Volume two-point flux dispatch (compile-time kind).
-template <int D, int VF, int AXIS, int MODE, int LOGS, int NX>
+template <int D, int VF, int AXIS, int MODE, int LOGS, int EH = 0, int NX>
 __device__ __forceinline__ void volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                             const Gas& gas, int pre, double* f, unsigned vm)
 {
-    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS>(l, r, nrm, gas.igm1, f, vm);
+    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS, EH>(l, r, nrm, gas.igm1, f, vm);
     else if constexpr (VF == F_SHIMA) flux_shima<D, AXIS, MODE>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_RANOCHA) flux_ranocha<D, AXIS, MODE, LOGS>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_CENTRAL) flux_central<D, AXIS, MODE>(l, r, nrm, gas.igm1, pre != PRE_NONE, f);

@@ -62,6 +62,7 @@ struct KParams {
                               // halo kernels: a full-occupancy grid holds every register of every SM)
     long long elem_base;      // added to element indices reported by the gate
     double wts[3][64];        // per direction: Dsplit[a,b] * Ja^n_n (Cartesian) or Dsplit (curved)
+    double wtsE[3][64];       // 2 * wts: the energy row of FAST fluxes that return f_E / 2 (energy_half)
     double areas[3];          // Cartesian Ja^n_n
     double jac_const;         // Cartesian J
     double rjac_const;        // 1/J (FAST)
@@ -91,7 +92,7 @@ struct KParams {
 #define FDG_MIN_BLOCKS 0  // 0: per-degree default below
 #endif
 #ifndef FDG_LINE_REGS
-#define FDG_LINE_REGS 0
+#define FDG_LINE_REGS 1  // compile-time passes: the line's node data in registers (r02: cfg5 VOL 3.52 -> 3.49 ms)
 #endif
 #ifndef FDG_STAGE_UNROLL
 #define FDG_STAGE_UNROLL 1
@@ -471,6 +472,7 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
             // creation), so the reference's pair table visits every pair
             const double wa = prm.wts[N][a * P1 + b];
             const double wb = prm.wts[N][b * P1 + a];
+            constexpr int EH = (MODE == FAST && energy_half(VF)) ? 1 : 0;
 #if FDG_LINE_REGS
             const Node<D, NX>& qb = qline[b];
 #else
@@ -481,14 +483,18 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
                 double alpha[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) alpha[j] = 0.5 * (jl[a][j] + jl[b][j]);
-                volume_flux<D, VF, -1, MODE, LOGS>(qa, qb, alpha, prm.gas, prm.precompute, f, vm);
+                volume_flux<D, VF, -1, MODE, LOGS, EH>(qa, qb, alpha, prm.gas, prm.precompute, f, vm);
             } else {
-                volume_flux<D, VF, N, MODE, LOGS>(qa, qb, nullptr, prm.gas, prm.precompute, f, vm);
+                volume_flux<D, VF, N, MODE, LOGS, EH>(qa, qb, nullptr, prm.gas, prm.precompute, f, vm);
             }
 #pragma unroll
-            for (int v = 0; v < NVAR; ++v) {
+            for (int v = 0; v < NVAR - EH; ++v) {
                 acc[a][v] += wa * f[v];
                 acc[b][v] += wb * f[v];
+            }
+            if constexpr (EH) {  // f[NVAR-1] = f_E / 2, weights doubled: the same product, exactly
+                acc[a][NVAR - 1] += prm.wtsE[N][a * P1 + b] * f[NVAR - 1];
+                acc[b][NVAR - 1] += prm.wtsE[N][b * P1 + a] * f[NVAR - 1];
             }
         });
     });
@@ -587,6 +593,8 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
         return q;
     };
     const double* w = prm.wts[n];
+    constexpr int EH = energy_half(VF) ? 1 : 0;
+    [[maybe_unused]] const double* wE = prm.wtsE[n];
     // FDG_FACE_EARLY: where the neighbour-trace loads of the fused interface
     // terms are issued -- 0: after the pair loop (with the fluxes), 1: before
     // the last pair (one flux evaluation hides the L2 latency), 2: before
@@ -617,14 +625,18 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
                 for (int j = 0; j < D; ++j)
                     alpha[j] = 0.5 * (__ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j) +
                                       __ldg(prm.ja + ((e * G::NN + base + b * stride) * D + n) * D + j));
-                fast_volume_flux<D, VF, -1, LOGS>(qa, qb, alpha, prm.gas.igm1, f, vm);
+                fast_volume_flux<D, VF, -1, LOGS, EH>(qa, qb, alpha, prm.gas.igm1, f, vm);
             } else {
-                fast_volume_flux<D, VF, 0, LOGS>(qa, qb, nullptr, prm.gas.igm1, f, vm);
+                fast_volume_flux<D, VF, 0, LOGS, EH>(qa, qb, nullptr, prm.gas.igm1, f, vm);
             }
 #pragma unroll
-            for (int v = 0; v < NVAR; ++v) {
+            for (int v = 0; v < NVAR - EH; ++v) {
                 acc[a][v] = fma(wa, f[v], acc[a][v]);
                 acc[b][v] = fma(wb, f[v], acc[b][v]);
+            }
+            if constexpr (EH) {
+                acc[a][NVAR - 1] = fma(wE[a * P1 + b], f[NVAR - 1], acc[a][NVAR - 1]);
+                acc[b][NVAR - 1] = fma(wE[b * P1 + a], f[NVAR - 1], acc[b][NVAR - 1]);
             }
         });
     });
@@ -1014,7 +1026,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                 // the gate's rare paths leave the node loop: its body is
                 // straight-line arithmetic that ptxas can interleave
                 unsigned slow = 0;                     // FAST: nodes needing the reference pressure test
-                unsigned long long bad = ~0ull;        // first failing flat node of this thread
+                unsigned bad = ~0u;                    // first failing flat node of this thread (batch-local index)
 #pragma unroll(kStageUnroll)
                 for (int k = 0; k < KN; ++k) {
                     const int t = tid + k * NT;
@@ -1025,9 +1037,9 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                         if constexpr (MODE == FAST) {
                             const int g = gate_fast<D>(su, 2.0 * q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
                             slow |= (g < 0) ? (1u << k) : 0u;
-                            bad = (g == 0 && (unsigned long long)t < bad) ? (unsigned long long)t : bad;
+                            bad = (g == 0 && (unsigned)t < bad) ? (unsigned)t : bad;
                         } else {
-                            bad = (!gate_ok<D>(su, prm.gas.gm1) && (unsigned long long)t < bad) ? (unsigned long long)t : bad;
+                            bad = (!gate_ok<D>(su, prm.gas.gm1) && (unsigned)t < bad) ? (unsigned)t : bad;
                         }
                         store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
                     }
@@ -1036,11 +1048,11 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
 #pragma unroll 1
                     for (int k = 0; k < KN; ++k) {
                         const int t = tid + k * NT;
-                        if (((slow >> k) & 1u) && !gate_ok<D>(sacc + t * NVAR, prm.gas.gm1) && (unsigned long long)t < bad)
-                            bad = t;
+                        if (((slow >> k) & 1u) && !gate_ok<D>(sacc + t * NVAR, prm.gas.gm1) && (unsigned)t < bad)
+                            bad = (unsigned)t;
                     }
                 }
-                if (bad != ~0ull) atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN) + bad);
+                if (bad != ~0u) atomicMin(&prm.status->first_bad, (unsigned long long)((prm.elem_base + e0) * NN) + bad);
             }
             __syncthreads();
             FDG_PT(1)
