@@ -182,7 +182,7 @@ int fdg_mesh_create(const fdg_mesh_desc_t* desc, fdg_mesh_t** out)
         m->dyn_claim = env ? atoi(env) : 2;
         // (round 2: the volume integral claims dynamically too: cfg5 VOL 3.87 -> 3.57 ms)
         k.claim_chunk_max = 1;
-        k.claim_chunk = 1;
+        k.zero = 0;
         // runtime-direction volume pass in the p+1 <= 4 interface kernels:
         // measured slower (cfg5 RHS 9.42 vs 8.92 ms with dynamic claiming,
         // profiles/r02_ab_rt_dc.txt), off by default
@@ -258,8 +258,27 @@ static LaunchFn find(const fdg_mesh* m, const fdg_scheme_t* s, int vf)
     return fn(vf, m->curved, logs);
 }
 
+// FAST launches on Cartesian meshes: 1/J folded into the pair weights and the
+// lift factors once per launch on the host (196 multiplies), so the
+// accumulators already hold VOL (and the fused interface lifts f / (w J)) and
+// the kernels' epilogue has no per-node scaling pass. FAITHFUL keeps the
+// reference's acc / J division.
+static void fold_jacobian(const fdg_mesh* m, const fdg_scheme_t* s, KParams& k)
+{
+    if (s->mode == FDG_MODE_FAITHFUL || m->curved || k.jac_folded) return;
+    for (int n = 0; n < 3; ++n)
+        for (int i = 0; i < 64; ++i) {
+            k.wts[n][i] *= k.rjac_const;
+            k.wtsE[n][i] *= k.rjac_const;
+        }
+    k.inv_w0 *= k.rjac_const;
+    k.inv_wp *= k.rjac_const;
+    k.jac_folded = 1;
+}
+
 static int run(fdg_mesh* m, const fdg_scheme_t* s, KParams& k, int vf, void* stream)
 {
+    fold_jacobian(m, s, k);
     k.claim = (m->dyn_claim >= 2 || (m->dyn_claim == 1 && k.epilogue != EPI_VOLUME)) ? m->claim : nullptr;
     k.reserve_sms = (k.epilogue != EPI_VOLUME) ? m->reserve_sms : 0;
     LaunchFn fn = find(m, s, vf);
@@ -313,6 +332,7 @@ static int volume_range(fdg_mesh* m, const fdg_scheme_t* s, LaunchFn fn, const d
     k.epilogue = EPI_VOLUME;
     k.precompute = s->precompute;
     k.surface_flux = F_LLF;
+    fold_jacobian(m, s, k);
     cudaError_t err = fn(k, stream, m->sm_count);
     if (err != cudaSuccess) return cuda_fail(err, "element kernel launch");
     g_launches.fetch_add(1);

@@ -226,11 +226,11 @@ namespace fdg {
 // Stage one node: primitives + the extras the volume flux needs.
 // FAITHFUL: (rho, v, p) exactly as cons2prim computes them;
 // FAST: (rho, v/2, p/2) -- see fdg_fast.cuh.
-template <int D, int VF, int MODE, int LOGS>
+template <int D, int VF, int MODE, int LOGS, int TAB = 0>
 __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node(const double* u, double gm1)
 {
     constexpr int NX = n_extra(VF, LOGS);
-    if constexpr (MODE == FAST) return make_node_fast<D, VF, LOGS>(u, gm1);
+    if constexpr (MODE == FAST) return make_node_fast<D, VF, LOGS, TAB>(u, gm1);
     Node<D, NX> q;
     cons2prim<D, MODE>(u, q.rho, q.v, q.p, gm1);
     if constexpr (VF == F_RANOCHA && LOGS) {

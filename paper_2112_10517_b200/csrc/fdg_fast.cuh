@@ -25,6 +25,8 @@
 // relative differences ~1e-15, tests/test_gpu_parity.py).
 #pragma once
 
+#include "fdg_logtab_fast.h"
+
 namespace fdg {
 
 // Literal FP64 constants of the FAST path live in the constant bank, where
@@ -107,6 +109,46 @@ __device__ __forceinline__ double log_fast_normal(double x)
     const double ed = (double)e;
     return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
 }
+// Table log for positive, normal, finite arguments (the per-node log tables
+// of the staging pass): x = 2^E m, i = top 7 mantissa bits, r_i = RN(128 /
+// (128 + i)), f = fma(m, r_i, -1) in [0, 2^-7), log x = k ln2 + T_i +
+// log1p(f) with T_i = -ln(r_i) - [i >= 53] ln2 and k = E + [i >= 53] (exact
+// identity for the stored r_i; scripts/gen_logtab_fast.py writes the table
+// and checks <= 1.5 ulp of max(|log x|, 2^-7) against 60-digit logs).
+// log1p(f) = f + f^2 P(f), Taylor to f^7 (truncation < 1.8e-18). 12 FP64
+// instructions and one 16-byte L1-resident load instead of 21 + a MUFU
+// reciprocal for log_fast_normal.
+#ifndef FDG_LOG_TAB
+#define FDG_LOG_TAB 1
+#endif
+__device__ __forceinline__ double log_tab(double x)
+{
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const int i = (hi >> 13) & 127;
+    const int k = ((hi + (75 << 13)) >> 20) - 1023;
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 rt = __ldg(&fdg_logtab_fast[i]);
+    const double f = fma(m, rt.x, -1.0);
+    const double f2 = f * f;
+    const double p01 = fma(1.0 / 3.0, f, -0.5);
+    const double p23 = fma(0.2, f, -0.25);
+    const double p45 = fma(1.0 / 7.0, f, -1.0 / 6.0);
+    const double p = fma(fma(p45, f2, p23), f2, p01);
+    const double l1p = fma(f2, p, f);
+    const double kd = (double)k;
+    return fma(kd, kFast[KC_LN2_HI], rt.y) + fma(kd, kFast[KC_LN2_LO], l1p);
+}
+// TAB: the volume-only twin takes the table log (cfg5 VOL 3.37 -> 3.31 ms);
+// in the RHS / stage twins its loads compete with the interface traces for
+// L1 and it measured 2% slower (5.37 vs 5.26 ms), so they keep the polynomial
+template <int TAB>
+__device__ __forceinline__ double log_node(double x)
+{
+    if constexpr (FDG_LOG_TAB && TAB) return log_tab(x);
+    else return log_fast_normal(x);
+}
+
 // x positive, normal, finite: one unsigned compare on the high word
 __device__ __forceinline__ bool log_normal_ok(double x)
 {
@@ -312,7 +354,7 @@ __device__ __forceinline__ void fast_central(const Node<D, NX>& l, const Node<D,
 }
 
 // FAST staging: rho, v/2, p/2 and the extras
-template <int D, int VF, int LOGS>
+template <int D, int VF, int LOGS, int TAB = 0>
 __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const double* u, double gm1)
 {
     constexpr int NX = n_extra(VF, LOGS);
@@ -334,8 +376,8 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     // states the gate reports, or absurdly scaled ones)
     if constexpr (VF == F_RANOCHA && LOGS) {
         const double a = 4.0 * q.p * hri;  // X = log(rho / p) = -log(2 ph / rho), 2 hri = 1/rho
-        q.x[0] = log_fast_normal(rho);
-        q.x[1] = -log_fast_normal(a);
+        q.x[0] = log_node<TAB>(rho);
+        q.x[1] = -log_node<TAB>(a);
         if (!(log_normal_ok(rho) && log_normal_ok(a))) {
             q.x[0] = log_fast(rho);
             q.x[1] = -log_fast(a);
@@ -343,8 +385,8 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     } else if constexpr (VF == F_CHANDRASHEKAR) {
         q.x[0] = 0.25 * rho * rcp_fast(q.p);  // beta = rho / (2 p)
         if constexpr (LOGS) {
-            q.x[1] = log_fast_normal(rho);
-            q.x[2] = log_fast_normal(q.x[0]);
+            q.x[1] = log_node<TAB>(rho);
+            q.x[2] = log_node<TAB>(q.x[0]);
             if (!(log_normal_ok(rho) && log_normal_ok(q.x[0]))) {
                 q.x[1] = log_fast(rho);
                 q.x[2] = log_fast(q.x[0]);

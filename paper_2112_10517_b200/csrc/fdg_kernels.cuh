@@ -55,8 +55,8 @@ struct KParams {
     long long range2_lo;      // optional second range [range2_lo, range2_hi) in the same launch
     long long range2_hi;      //   (both boundary planes of a slab in one launch); empty by default
     unsigned long long* claim; // dynamic batch claiming: [0] next batch, [1] CTAs done (null: static grid-stride)
-    int claim_chunk;          // (unused since claims are per batch, one ahead; kept for the parameter-block layout)
-    int claim_chunk_max;
+    int zero;                 // always 0 (claim_batch: keeps the claim's address from being provably uniform)
+    int claim_chunk_max;      // (unused since claims are per batch, one ahead)
     int rt_iface;             // interface epilogues below FDG_RT_DIR_MIN_P1 take the runtime-direction pass
     int reserve_sms;          // launch only on sm_count - reserve_sms SMs' worth of CTAs (room for concurrent
                               // halo kernels: a full-occupancy grid holds every register of every SM)
@@ -69,6 +69,7 @@ struct KParams {
     double w0, wp;            // LGL weights at the -1 / +1 ends
     double inv_w0, inv_wp;    // 1/w0, 1/wp (FAST: interface terms fused into the volume passes)
     int fuse_faces;           // FAST RHS / RK-stage launches with the Rusanov interface flux: line-end fusion on
+    int jac_folded;           // FAST Cartesian launches: wts / wtsE / inv_w0 / inv_wp already carry 1/J (fdg_capi.cu)
     Gas gas;
     int epilogue;
     int surface_flux;
@@ -252,6 +253,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
         "}\n" ::"r"(b),
         "r"(phase)
         : "memory");
+}
+
+// one batch claim by thread 0, result left in flight. nvcc and ptxas turn an
+// atomic add on a uniform address into the warp-aggregated form (leader
+// election, one ATOMG, SHFL broadcast of the result), and the shuffle waits
+// for the atomic right away: 2.7% of the cfg5 VOL stall samples sat on it
+// (r02_v6 capture). The address is therefore offset by (laneid & zero) with
+// the lane id read through volatile asm and `zero` a kernel parameter that is
+// always 0: not provably uniform, so the plain instruction is emitted and
+// its result is only waited for at the end of the batch.
+__device__ __forceinline__ long long claim_batch(unsigned long long* counter, int zero)
+{
+    unsigned lane;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+    unsigned long long r;
+    asm volatile("atom.global.add.u64 %0, [%1], 1;" : "=l"(r) : "l"(counter + (lane & (unsigned)zero)) : "memory");
+    return (long long)r;
 }
 
 // compile-time for loop: f(integral_constant<int, i>) for i in [B, E)
@@ -892,8 +910,8 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     [[maybe_unused]] long long pending = 0;
     if (dyn) {
         if (tid == 0) {
-            s_claim[0] = (long long)atomicAdd(prm.claim, 1ull);
-            s_claim[1] = (long long)atomicAdd(prm.claim, 1ull);
+            s_claim[0] = claim_batch(prm.claim, prm.zero);
+            s_claim[1] = claim_batch(prm.claim, prm.zero);
         }
         __syncthreads();
         batch = s_claim[0];
@@ -911,7 +929,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         next = s_claim[0];
     };
     for (; batch < nbatch; advance()) {
-        if (dyn && tid == 0) pending = (long long)atomicAdd(prm.claim, 1ull);
+        if (dyn && tid == 0) pending = claim_batch(prm.claim, prm.zero);
         const long long e0 = first(batch);
         const int ne = (int)min((long long)EPB, range_end(batch) - e0);
         const long long base = e0 * NN * NVAR;
@@ -1033,7 +1051,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                     if (t < ne * NN) {
                         const int tel = t / NN, node = t - tel * NN;
                         const double* su = sacc + t * NVAR;
-                        const Node<D, NX> q = make_node<D, VF, MODE, LOGS>(su, prm.gas.gm1);
+                        const Node<D, NX> q = make_node<D, VF, MODE, LOGS, EPIK == EPI_VOLUME>(su, prm.gas.gm1);
                         if constexpr (MODE == FAST) {
                             const int g = gate_fast<D>(su, 2.0 * q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
                             slow |= (g < 0) ? (1u << k) : 0u;
@@ -1105,14 +1123,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                 if (t < ne * NN) {
                     const int tel = t / NN, node = t - tel * NN;
                     double scale;
+                    // (FAST Cartesian: 1/J is already in the weights, fold_jacobian)
                     if constexpr (MODE == FAST)
-                        scale = CURVED ? rcp_fast(__ldg(prm.jac + e0 * NN + t)) : prm.rjac_const;
+                        scale = CURVED ? rcp_fast(__ldg(prm.jac + e0 * NN + t)) : 1.0;
                     else
                         scale = CURVED ? __ldg(prm.jac + e0 * NN + t) : prm.jac_const;
 #pragma unroll
                     for (int v = 0; v < NVAR; ++v) {
                         const int s = G::acc(v, tel, node);
-                        const double vol = (MODE == FAST) ? sacc[s] * scale : sacc[s] / scale;
+                        const double vol = (MODE == FAST) ? (CURVED ? sacc[s] * scale : sacc[s]) : sacc[s] / scale;
                         if (epi == EPI_VOLUME) {
                             if (tma_out) sq[t * NVAR + v] = vol;  // AoS, conflict-free (odd stride)
                             else prm.out[base + t * NVAR + v] = vol;

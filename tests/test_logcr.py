@@ -56,3 +56,21 @@ def test_glibc_log_is_not_correctly_rounded_here():
     xs = rng.uniform(0.2, 5.0, 20000).tolist()
     mis = sum(1 for x in xs if math.log(x) != _cr(x))
     assert 0 < mis < 0.01 * len(xs)
+
+
+def test_fast_table_log_accuracy_and_header():
+    """log_tab (the per-node table log of the FAST volume-only kernels,
+    csrc/fdg_fast.cuh): the device algorithm re-run in exactly rounded
+    arithmetic stays within 1.5 ulp of max(|log x|, 2^-7) of 60-digit logs,
+    and the committed table is what scripts/gen_logtab_fast.py generates."""
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen_logtab_fast", os.path.join(root, "scripts", "gen_logtab_fast.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    with open(gen.HEADER) as fh:
+        assert fh.read() == gen.header_text()
+    worst, n = gen.max_error_ulps(n=1500, seed=7)
+    assert n > 4000 and worst < 1.6
