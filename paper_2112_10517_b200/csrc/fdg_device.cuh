@@ -202,19 +202,33 @@ __device__ __forceinline__ bool gate_ok(const double* u, double gm1)
 // pressure p_fast and the gate's pressure differ by a few ulps of
 // (gamma-1) max(|E|, kinetic); whenever |p_fast| exceeds 1e-10 (gamma-1)|E|
 // their signs agree, otherwise the gate's own formula decides.
+#ifndef FDG_STAGE_LEAN
+#define FDG_STAGE_LEAN 1  // integer finite / sign tests in gate_fast, half pressure in, negated table log
+#endif
+// p_half: the staged FAST half pressure p/2
 template <int D>
-__device__ __forceinline__ int gate_fast(const double* u, double p_fast, double gm1)
+__device__ __forceinline__ int gate_fast(const double* u, double p_half, double gm1)
 {
     // 1: admissible, 0: not, -1: |p| too close to 0 for the FAST pressure's
     // sign to be trusted -> the caller re-runs gate_ok (reference formula)
     // rho positive, normal and finite in one unsigned compare on its high
     // word (a positive subnormal density goes to the reference test); an
-    // infinite or NaN p_fast fails the magnitude comparison's finite side
+    // infinite or NaN p fails the magnitude comparison's finite side
     const double rho = u[0];
     const bool rho_ok = (unsigned)(__double2hiint(rho) - 0x00100000) < 0x7fe00000u;
+#if FDG_STAGE_LEAN
+    // |p/2| finite and the sign of p on the high word (integer pipe); one
+    // FP64 compare for the magnitude: |p/2| > (1e-10/2) (gamma-1) |E|
+    const int hi = __double2hiint(p_half);
+    const bool finite = (unsigned)(hi & 0x7fffffff) < 0x7ff00000u;
+    const bool clear = rho_ok && finite && fabs(p_half) > (0.5e-10 * gm1) * fabs(u[D + 1]);
+    return clear ? (hi >= 0 ? 1 : 0) : -1;
+#else
+    const double p_fast = 2.0 * p_half;
     const double ap = fabs(p_fast);
     const bool clear = rho_ok && ap <= 1.7976931348623157e308 && ap > 1e-10 * gm1 * fabs(u[D + 1]);
     return clear ? (p_fast > 0.0 ? 1 : 0) : -1;
+#endif
 }
 
 }  // namespace fdg
@@ -611,6 +625,80 @@ __device__ __forceinline__ void flux_llf_fast(const double* ul, const double* ur
 // interface then evaluate the flux from differently rounded copies of each
 // other's state (staged primitives vs conserved), so the two lifted values
 // agree to rounding (~1e-16 relative), not to the bit.
+#ifndef FDG_LLF_OWN_LEAN
+#define FDG_LLF_OWN_LEAN 1
+#endif
+#if FDG_LLF_OWN_LEAN
+// Every 1/2 of the Rusanov flux is taken from the half-staged own values or
+// folded into a uniform constant: own momenta as (2 rho) (v/2), the half
+// normal mass-flux factors v.n/2 straight from v/2 (own) and from the halved
+// normal (neighbour), the half pressures summed for the pressure term --
+// 69 instead of 78 FP64 instructions per flux (3D, axis aligned), same value
+// up to the rounding of the rearranged products.
+template <int D, int AXIS, bool OWN_LEFT>
+__device__ __forceinline__ void flux_llf_fast_own(double orho, const double* ovh, double oph, const double* un,
+                                                  const double* nrm, const Gas& gas, double* f)
+{
+    // own side from the staged values
+    const double r2 = 2.0 * orho;
+    double om[D], s = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        om[i] = r2 * ovh[i];
+        s = fma(ovh[i], ovh[i], s);
+    }
+    const double oE = fma(r2, s, oph * (2.0 * gas.igm1));  // rho |v|^2 / 2 + p / (gamma - 1)
+    // neighbour side from its conserved trace
+    const double rin = rcp_fast(un[0]);
+    double nv[D], kn = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        nv[i] = un[1 + i] * rin;
+        kn = fma(un[1 + i], nv[i], kn);
+    }
+    const double nph = (0.5 * gas.gm1) * fma(-0.5, kn, un[D + 1]);  // p_n / 2
+    // ohv, nhv: v.n / 2 with the scaled normal; olam, nlam: |v.n|/|n| + c
+    double norm, ohv, nhv, olam, nlam;
+    // c = sqrt(gamma p / rho) = gamma p rsqrt(gamma p rho): no reciprocal of the own density
+    const double g2 = 2.0 * gas.gamma;
+    const double ogp = g2 * oph, ngp = g2 * nph;
+    const double oc = ogp * rsqrt_fast(ogp * orho), nc = ngp * rsqrt_fast(ngp * un[0]);
+    if constexpr (AXIS >= 0) {
+        norm = nrm[AXIS];
+        ohv = ovh[AXIS] * norm;
+        nhv = nv[AXIS] * (0.5 * norm);
+        olam = fma(2.0, fabs(ovh[AXIS]), oc);
+        nlam = nc + fabs(nv[AXIS]);
+    } else {
+        double nn = 0.0, nvn = 0.0;
+        ohv = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            nn = fma(nrm[i], nrm[i], nn);
+            ohv = fma(ovh[i], nrm[i], ohv);
+            nvn = fma(nv[i], nrm[i], nvn);
+        }
+        const double inorm_ = rsqrt_fast(nn);
+        norm = nn * inorm_;
+        nhv = 0.5 * nvn;
+        olam = fma(fabs(ohv), 2.0 * inorm_, oc);
+        nlam = fma(fabs(nvn), inorm_, nc);
+    }
+    const double hd = 0.5 * fmax(olam, nlam) * norm;
+    const double sg = OWN_LEFT ? hd : -hd;  // -halfdiss (u_r - u_l) = sg (own - neighbour)
+    const double hp = oph + nph;            // {p}
+    f[0] = fma(sg, orho - un[0], fma(orho, ohv, un[0] * nhv));
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double c = fma(om[i], ohv, un[1 + i] * nhv);
+        double cp;
+        if constexpr (AXIS >= 0) cp = (i == AXIS) ? fma(hp, norm, c) : c;
+        else cp = fma(hp, nrm[i], c);
+        f[1 + i] = fma(sg, om[i] - un[1 + i], cp);
+    }
+    f[D + 1] = fma(sg, oE - un[D + 1], fma(fma(2.0, oph, oE), ohv, fma(2.0, nph, un[D + 1]) * nhv));
+}
+#else
 template <int D, int AXIS, bool OWN_LEFT>
 __device__ __forceinline__ void flux_llf_fast_own(double orho, const double* ovh, double oph, const double* un,
                                                   const double* nrm, const Gas& gas, double* f)
@@ -675,6 +763,8 @@ __device__ __forceinline__ void flux_llf_fast_own(double orho, const double* ovh
     }
     f[D + 1] = fma(sg, oE - un[D + 1], 0.5 * fma(oE + op, ovns, (un[D + 1] + np_) * nvns));
 }
+
+#endif
 
 // Two-point flux with conserved inputs for the interface (runtime kind).
 template <int D, int MODE>

@@ -89,6 +89,9 @@ __device__ __forceinline__ double log_fast(double x)
 // The same log for arguments known to be positive, normal and finite: no
 // subnormal rescale, no special-value selects (17 fewer instructions per
 // call). Bitwise equal to log_fast there. log_normal_ok(x) is the test.
+// NEG: returns -log x with the sign folded into operand negations of the last
+// two FMAs (exactly the negated value, no extra instruction)
+template <bool NEG = false>
 __device__ __forceinline__ double log_fast_normal(double x)
 {
     const int hi = __double2hiint(x);
@@ -107,7 +110,8 @@ __device__ __forceinline__ double log_fast_normal(double x)
     const double p = fma(p47, z2 * z2, p03);
     const double corr = s * fma(-z, p, f);
     const double ed = (double)e;
-    return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
+    if constexpr (NEG) return fma(-ed, kFast[KC_LN2_HI], -f) + fma(-ed, kFast[KC_LN2_LO], corr);
+    else return fma(ed, kFast[KC_LN2_HI], f) + fma(ed, kFast[KC_LN2_LO], -corr);
 }
 // Table log for positive, normal, finite arguments (the per-node log tables
 // of the staging pass): x = 2^E m, i = top 7 mantissa bits, r_i = RN(128 /
@@ -121,6 +125,7 @@ __device__ __forceinline__ double log_fast_normal(double x)
 #ifndef FDG_LOG_TAB
 #define FDG_LOG_TAB 1
 #endif
+template <bool NEG = false>
 __device__ __forceinline__ double log_tab(double x)
 {
     const int hi = __double2hiint(x);
@@ -137,16 +142,17 @@ __device__ __forceinline__ double log_tab(double x)
     const double p = fma(fma(p45, f2, p23), f2, p01);
     const double l1p = fma(f2, p, f);
     const double kd = (double)k;
-    return fma(kd, kFast[KC_LN2_HI], rt.y) + fma(kd, kFast[KC_LN2_LO], l1p);
+    if constexpr (NEG) return fma(-kd, kFast[KC_LN2_HI], -rt.y) + fma(-kd, kFast[KC_LN2_LO], -l1p);
+    else return fma(kd, kFast[KC_LN2_HI], rt.y) + fma(kd, kFast[KC_LN2_LO], l1p);
 }
 // TAB: the volume-only twin takes the table log (cfg5 VOL 3.37 -> 3.31 ms);
 // in the RHS / stage twins its loads compete with the interface traces for
 // L1 and it measured 2% slower (5.37 vs 5.26 ms), so they keep the polynomial
-template <int TAB>
+template <int TAB, bool NEG = false>
 __device__ __forceinline__ double log_node(double x)
 {
-    if constexpr (FDG_LOG_TAB && TAB) return log_tab(x);
-    else return log_fast_normal(x);
+    if constexpr (FDG_LOG_TAB && TAB) return log_tab<NEG>(x);
+    else return log_fast_normal<NEG>(x);
 }
 
 // x positive, normal, finite: one unsigned compare on the high word
@@ -163,6 +169,27 @@ __device__ __forceinline__ bool log_normal_ok(double x)
 // u < 1e-4); dl is exact up to the rounding of the two logs
 __device__ __forceinline__ bool series_test(double dl) { return fabs(dl) < kFast[KC_SERIES_DL]; }
 
+// FDG_LM_LEAN (r02 session 5): the same two candidates with fewer
+// instructions per log mean --
+//   * the branch test on the high word of z = dl^2 (z >= 0: one integer
+//     compare, no FP64-pipe DSETP; the threshold moves by < 2^-20 relative,
+//     and both candidates are accurate around it);
+//   * num = fma(sgn, a, b) with sgn = +-1 selected in the high word only
+//     (b + a on series lanes, b - a otherwise, the same bits as the two
+//     separate sums): one select + one DFMA instead of a negation, an add
+//     and a two-word select;
+//   * FDG_CT_TERMS = 2 drops the z^3/15120 term of 2 x coth x: below the
+//     threshold z < 4.0003e-4 it is < 4.3e-15 of the mean (the log candidate
+//     just above the threshold carries ~1e-14 from the rounding of dl).
+#ifndef FDG_LM_LEAN
+#define FDG_LM_LEAN 1
+#endif
+#ifndef FDG_CT_TERMS
+#define FDG_CT_TERMS 2
+#endif
+// high word of KC_SERIES_DL^2 = 4.000266687e-4 (0x3F3A375575AB25FF): z below it <=> series
+constexpr int kSeriesZHi = 0x3F3A3755;
+
 // <a,b>_log = num / den: the log branch (num, den) = (b - a, dl) is the
 // caller's; on series lanes it becomes (a + b, 2 x coth x), x = dl/2.
 // With t = (b-a)/(b+a) = tanh(x), <a,b>_log = (b-a)/dl = (a+b) tanh(x)/(2x)
@@ -170,19 +197,41 @@ __device__ __forceinline__ bool series_test(double dl) { return fabs(dl) < kFast
 // function of t.  2 x coth x = 2 + z/6 - z^2/360 + z^3/15120 - ..., z = dl^2:
 // dl enters only through the O(z) corrections, so its rounding (which is why
 // (b-a)/dl fails for b ~ a) costs nothing, and no reciprocal is needed
-// (truncation < 1e-19 relative for |dl| < 0.02).
+// (truncation < 1e-19 relative for |dl| < 0.02 with three terms).
+__device__ __forceinline__ double coth_series(double z)
+{
+#if FDG_CT_TERMS >= 3
+    return fma(z, fma(z, fma(z, kFast[KC_CT3], kFast[KC_CT2]), kFast[KC_CT1]), 2.0);
+#else
+    return fma(z, fma(z, kFast[KC_CT2], kFast[KC_CT1]), 2.0);
+#endif
+}
 __device__ __forceinline__ void series_frac(double a, double b, double dl, bool series, double& num, double& den)
 {
     const double z = dl * dl;
-    const double cth = fma(z, fma(z, fma(z, kFast[KC_CT3], kFast[KC_CT2]), kFast[KC_CT1]), 2.0);
+    const double cth = coth_series(z);
     num = series ? b + a : num;
     den = series ? cth : den;
+}
+// lean form: (num, den) of one log mean from scratch
+__device__ __forceinline__ void logmean_frac(double a, double b, double dl, double& num, double& den)
+{
+    const double z = dl * dl;
+    const bool series = __double2hiint(z) < kSeriesZHi;
+    const double cth = coth_series(z);
+    const double sgn = __hiloint2double(series ? 0x3ff00000 : (int)0xbff00000, 0);
+    num = fma(sgn, a, b);
+    den = series ? cth : dl;
 }
 
 // both log means of a pair; the series work only when a lane of the warp needs it
 __device__ __forceinline__ void logmean_pair(double a1, double b1, double dl1, double& num1, double& den1, double a2,
                                              double b2, double dl2, double& num2, double& den2, unsigned vm)
 {
+#if FDG_LM_LEAN
+    logmean_frac(a1, b1, dl1, num1, den1);
+    logmean_frac(a2, b2, dl2, num2, den2);
+#else
     num1 = b1 - a1;
     den1 = dl1;
     num2 = b2 - a2;
@@ -196,6 +245,7 @@ __device__ __forceinline__ void logmean_pair(double a1, double b1, double dl1, d
         series_frac(a1, b1, dl1, s1, num1, den1);
         series_frac(a2, b2, dl2, s2, num2, den2);
     }
+#endif
 }
 
 // half-value dot products with the face/metric direction
@@ -377,7 +427,7 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     if constexpr (VF == F_RANOCHA && LOGS) {
         const double a = 4.0 * q.p * hri;  // X = log(rho / p) = -log(2 ph / rho), 2 hri = 1/rho
         q.x[0] = log_node<TAB>(rho);
-        q.x[1] = -log_node<TAB>(a);
+        q.x[1] = FDG_STAGE_LEAN ? log_node<TAB, true>(a) : -log_node<TAB>(a);
         if (!(log_normal_ok(rho) && log_normal_ok(a))) {
             q.x[0] = log_fast(rho);
             q.x[1] = -log_fast(a);

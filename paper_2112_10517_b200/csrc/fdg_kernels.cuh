@@ -890,8 +890,11 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     auto first = [&](long long b) -> long long {
         const long long f = b < nb1 ? prm.range_lo + b * EPB : prm.range2_lo + (b - nb1) * EPB;
         if (!remap) return f;
-        const long long r = f / prm.row_len;
-        return (long long)__ldg(prm.row_order + r) * prm.row_len + (f - r * prm.row_len);
+        // (element indices fit 31 bits -- the neighbour tables are int32 --
+        // so the row split is one 32-bit division)
+        const unsigned rl = (unsigned)prm.row_len;
+        const unsigned r = (unsigned)f / rl;
+        return (long long)__ldg(prm.row_order + r) * prm.row_len + ((unsigned)f - r * rl);
     };
 
     // batch assignment: static grid-stride, or dynamic claiming, one batch at
@@ -928,9 +931,12 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         batch = next;
         next = s_claim[0];
     };
-    for (; batch < nbatch; advance()) {
+    // first element of the current batch; the next batch's is computed once,
+    // for the L2 prefetch, and carried into the next iteration
+    long long e0_cur = batch < nbatch ? first(batch) : 0, e0_next = 0;
+    for (; batch < nbatch; advance(), e0_cur = e0_next) {
         if (dyn && tid == 0) pending = claim_batch(prm.claim, prm.zero);
-        const long long e0 = first(batch);
+        const long long e0 = e0_cur;
         const int ne = (int)min((long long)EPB, range_end(batch) - e0);
         const long long base = e0 * NN * NVAR;
         const int count = ne * NN * NVAR;
@@ -941,14 +947,16 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
         const bool tma = tma_u && (count % 2) == 0 && (base % 2) == 0;
         const bool tma_out = tma_out_ok && (count % 2) == 0 && (base % 2) == 0;
 
+        const long long nb_next = !dyn ? batch + gridDim.x : next;
+        if (nb_next < nbatch) e0_next = first(nb_next);
 #if FDG_PREFETCH
         // warm L2 with the next batch of this CTA (its state, and metrics on
         // curved meshes) while this one computes: the next staging copy then
         // waits on L2, not HBM, latency
         {
-            const long long nb = !dyn ? batch + gridDim.x : next;
+            const long long nb = nb_next;
             if (nb < nbatch) {
-                const long long f2 = first(nb);
+                const long long f2 = e0_next;
                 const long long ne2 = min((long long)EPB, range_end(nb) - f2);
                 const char* p0 = reinterpret_cast<const char*>(prm.u + f2 * NN * NVAR);
                 const int bytes = (int)(ne2 * NN * NVAR * 8);
@@ -1053,7 +1061,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                         const double* su = sacc + t * NVAR;
                         const Node<D, NX> q = make_node<D, VF, MODE, LOGS, EPIK == EPI_VOLUME>(su, prm.gas.gm1);
                         if constexpr (MODE == FAST) {
-                            const int g = gate_fast<D>(su, 2.0 * q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
+                            const int g = gate_fast<D>(su, q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
                             slow |= (g < 0) ? (1u << k) : 0u;
                             bad = (g == 0 && (unsigned)t < bad) ? (unsigned)t : bad;
                         } else {
