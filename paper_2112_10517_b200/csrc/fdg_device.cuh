@@ -48,10 +48,18 @@ constexpr double SERIES_EPSILON = 1.0e-4;  // means.py:16
 
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// FAST Ranocha nodes also carry b = rho / p: the (rho p) log mean becomes the
+// log mean of (b_l, b_r) -- <rho_l p_r, rho_r p_l>_log = p_l p_r <b_l, b_r>_log
+// by homogeneity -- so a pair forms neither rho_l p_r, rho_r p_l nor p_l p_r
+// (4 of 49 FP64 instructions per pair) for one more staged value per node.
+// The FAITHFUL kernels keep the reference's arguments and leave the slot unused.
+#ifndef FDG_RANOCHA_B
+#define FDG_RANOCHA_B 1
+#endif
 // number of extra per-node values a volume flux stages next to (rho, v, p)
 __host__ __device__ constexpr int n_extra(int vf, int logs)
 {
-    return vf == F_RANOCHA ? (logs ? 2 : 0)
+    return vf == F_RANOCHA ? (logs ? 2 : 0) + FDG_RANOCHA_B  // FAST: + b = rho / p (fdg_fast.cuh)
          : vf == F_CHANDRASHEKAR ? (logs ? 3 : 1)
          : vf == F_KG ? 1
          : vf == F_CENTRAL ? 5  // conserved state (rho, m1..m3 | E), padded to 5
@@ -247,9 +255,13 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node(const double* u,
     if constexpr (MODE == FAST) return make_node_fast<D, VF, LOGS, TAB>(u, gm1);
     Node<D, NX> q;
     cons2prim<D, MODE>(u, q.rho, q.v, q.p, gm1);
-    if constexpr (VF == F_RANOCHA && LOGS) {
-        q.x[0] = dlog<MODE>(q.rho);
-        q.x[1] = dlog<MODE>(q.p);
+    if constexpr (VF == F_RANOCHA) {
+#pragma unroll
+        for (int i = 0; i < (NX > 0 ? NX : 1); ++i) q.x[i] = 0.0;
+        if constexpr (LOGS) {
+            q.x[0] = dlog<MODE>(q.rho);
+            q.x[1] = dlog<MODE>(q.p);
+        }
     } else if constexpr (VF == F_CHANDRASHEKAR) {
         q.x[0] = q.rho / (2.0 * q.p);  // beta
         if constexpr (LOGS) {

@@ -21,10 +21,14 @@ template <int D, int P1, int MODE, bool CURVED>
 constexpr bool has_hiocc()
 {
     // (curved kernels spill heavily at 128 registers: no twin)
+    // (FDG_HIOCC counts 64-thread CTAs: only for kernels of that size)
     return FDG_HIOCC > 0 && MODE == FAST && D == 3 && P1 <= 5 && !CURVED && FDG_MIN_BLOCKS == 0 &&
-           min_blocks<D, P1, MODE, CURVED>() < FDG_HIOCC;
+           Geo<D, P1>::NT == 64 && min_blocks<D, P1, MODE, CURVED>() < FDG_HIOCC;
 }
 
+#ifndef FDG_VOLK_HIOCC
+#define FDG_VOLK_HIOCC 1
+#endif
 // Volume-integral-only twin (EPIK = EPI_VOLUME) of the FAST 3D kernels the
 // BASELINE volume workloads run: the image holds no interface / stage code.
 #ifndef FDG_VOLK
@@ -33,7 +37,7 @@ constexpr bool has_hiocc()
 template <int D, int P1, int MODE, bool CURVED>
 constexpr bool has_volk()
 {
-    return FDG_VOLK && MODE == FAST && D == 3 && (P1 == 4 || P1 == 5 || P1 == 8);  // BASELINE degrees N = 3, 4, 7
+    return FDG_VOLK && MODE == FAST && D == 3 && P1 >= 4;  // N = 3..7 (north-star degrees)
 }
 
 // RHS / RK-stage twins with the interface terms fused (Rusanov): no separate
@@ -141,7 +145,23 @@ cudaError_t launch_elem(const KParams& p_in, cudaStream_t s, int sm_count)
     if constexpr (has_volk<D, P1, MODE, CURVED>()) {
         if (p.epilogue == EPI_VOLUME) {
             static bool attr_set[kMaxDev] = {};
-            return launch_twin(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0, EPI_VOLUME>, attr_set);
+            if constexpr (twin && FDG_VOLK_HIOCC) {
+                // the volume-only twin of this degree (p + 1 = 5, Cartesian) is also the
+                // faster one at the high-occupancy register cap in steady state
+                // (N=4 VOL: Ranocha 2.27 -> 2.21 ms, Shima 1.63 -> 1.50 ms)
+                const long long slots_hi = (long long)bps_hi * std::max(1, sm_count - std::max(0, p.reserve_sms));
+                if (p_in.claim && nb > slots_hi) p.claim = p_in.claim;
+                else p.claim = nullptr;
+                auto kern = elem_kernel<D, P1, VF, CURVED, MODE, LOGS, FDG_HIOCC, EPI_VOLUME>;
+                if (dev >= 0 && dev < kMaxDev && !attr_set[dev]) {
+                    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    if (err != cudaSuccess) return err;
+                    attr_set[dev] = true;
+                }
+                return launch_kernel(kern, (unsigned)std::min(nb, slots_hi), G::NT, smem, s, p);
+            } else {
+                return launch_twin(elem_kernel<D, P1, VF, CURVED, MODE, LOGS, 0, EPI_VOLUME>, attr_set);
+            }
         }
     }
     if constexpr (has_rhsk<D, P1, VF, MODE, CURVED>()) {

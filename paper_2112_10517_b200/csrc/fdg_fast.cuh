@@ -278,6 +278,44 @@ __device__ __forceinline__ void fast_momentum(double f_rho, double p_avg, const 
 // EH = 1: f[D+1] comes back as f_E / 2 (the volume passes multiply it with
 // the doubled weight table wtsE: scaling by 2 is exact, so the accumulated
 // bits are the same and two multiplies per pair are gone)
+#if FDG_RANOCHA_B
+// x = (log rho, log b, b) with log tables, (b) without; b = rho / p.
+// f_rho = <rho>_log {v.n};  f_E = f_rho (v_l.v_r / 2 + igm1 / <b>_log) + (p_l vn_r + p_r vn_l) / 2
+// since p_l p_r / <rho_l p_r, rho_r p_l>_log = 1 / <b_l, b_r>_log.
+template <int D, int AXIS, int LOGS, int EH = 0, int NX>
+__device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
+                                             double igm1, double* f, unsigned vm)
+{
+    const double bl = l.x[LOGS ? 2 : 0], br = r.x[LOGS ? 2 : 0];
+    double dl1, dl2;
+    if constexpr (LOGS) {
+        dl1 = r.x[0] - l.x[0];  // log rho_r - log rho_l
+        dl2 = r.x[1] - l.x[1];  // log b_r - log b_l
+    } else {
+        dl1 = log_fast(r.rho * rcp_fast(l.rho));
+        dl2 = log_fast(br * rcp_fast(bl));
+    }
+    double num1, den1, num2, den2;  // <rho>_log = num1/den1, <b>_log = num2/den2
+    logmean_pair(l.rho, r.rho, dl1, num1, den1, bl, br, dl2, num2, den2, vm);
+    // everything that does not need the shared reciprocal is formed while
+    // MUFU + its correction run
+    const double vn_l = hdot<D, AXIS>(l.v, nrm);
+    const double vn_r = hdot<D, AXIS>(r.v, nrm);
+    const double pre_rho = num1 * num2 * (vn_l + vn_r);                 // f_rho / rr
+    const double pre_e = ((EH ? 0.5 : 1.0) * igm1) * (den1 * den2);     // (igm1 / <b>_log) / rr (EH: half of it)
+    double vv = l.v[0] * r.v[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) vv = fma(l.v[i], r.v[i], vv);
+    const double pv = fma(l.p, vn_r, r.p * vn_l);
+    const double rr = rcp_fast(den1 * num2);
+    const double f_rho = pre_rho * rr;
+    f[0] = f_rho;
+    // half values: vv = v_l.v_r / 4, pv = (p_l vn_r + p_r vn_l) / 4
+    if constexpr (EH) f[D + 1] = fma(f_rho, fma(pre_e, rr, vv), pv);
+    else f[D + 1] = fma(f_rho, fma(pre_e, rr, 2.0 * vv), 2.0 * pv);
+    fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
+}
+#else
 template <int D, int AXIS, int LOGS, int EH = 0, int NX>
 __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                              double igm1, double* f, unsigned vm)
@@ -315,6 +353,8 @@ __device__ __forceinline__ void fast_ranocha(const Node<D, NX>& l, const Node<D,
     else f[D + 1] = fma(f_rho, fma(pre_e, rr, 2.0 * vv), 2.0 * pv);
     fast_momentum<D, AXIS>(f_rho, l.p + r.p, l.v, r.v, nrm, f);
 }
+
+#endif
 
 template <int D, int AXIS, int NX>
 __device__ __forceinline__ void fast_shima(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
@@ -424,6 +464,20 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
     // states) positive-normal path, the full log_fast behind one rarely
     // taken branch for everything else (zero, negative, subnormal, inf, NaN:
     // states the gate reports, or absurdly scaled ones)
+#if FDG_RANOCHA_B
+    if constexpr (VF == F_RANOCHA) {
+        const double b = (0.5 * rho) * rcp_fast(q.p);  // rho / p
+        q.x[LOGS ? 2 : 0] = b;
+        if constexpr (LOGS) {
+            q.x[0] = log_node<TAB>(rho);
+            q.x[1] = log_node<TAB>(b);
+            if (!(log_normal_ok(rho) && log_normal_ok(b))) {
+                q.x[0] = log_fast(rho);
+                q.x[1] = log_fast(b);
+            }
+        }
+    } else if constexpr (VF == F_CHANDRASHEKAR) {
+#else
     if constexpr (VF == F_RANOCHA && LOGS) {
         const double a = 4.0 * q.p * hri;  // X = log(rho / p) = -log(2 ph / rho), 2 hri = 1/rho
         q.x[0] = log_node<TAB>(rho);
@@ -433,6 +487,7 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
             q.x[1] = -log_fast(a);
         }
     } else if constexpr (VF == F_CHANDRASHEKAR) {
+#endif
         q.x[0] = 0.25 * rho * rcp_fast(q.p);  // beta = rho / (2 p)
         if constexpr (LOGS) {
             q.x[1] = log_node<TAB>(rho);

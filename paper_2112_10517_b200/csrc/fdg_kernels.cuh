@@ -147,7 +147,21 @@ struct Geo {
 #define FDG_P4_TT 32
 #endif
     static constexpr int TT = (D == 3 && P1 == 4 && FDG_TARGET_THREADS == 64) ? FDG_P4_TT : FDG_TARGET_THREADS;
-    static constexpr int EPB = LINES >= TT ? 1 : TT / LINES;
+    // 3D p + 1 = 5, 6, 7: 25 / 36 / 49 lines per element leave 22-44% of a
+    // 64-thread CTA's lanes idle (FP64-bound degrees: lane utilisation is
+    // throughput); per-degree batch sizes, measured (profiles/r02_tuning.md).
+    // Even EPB * NN * NVAR keeps every batch 16-byte aligned for the bulk copies.
+#ifndef FDG_EPB_P5
+#define FDG_EPB_P5 0  // 0: TT / LINES (2 elements, 50 of 64 lanes: larger batches measured slower, r02_tuning.md)
+#endif
+#ifndef FDG_EPB_P6
+#define FDG_EPB_P6 3  // 108 of 128 lanes (1 element: 36 of 64)
+#endif
+#ifndef FDG_EPB_P7
+#define FDG_EPB_P7 2  // 98 of 128 lanes, 4-warp CTAs
+#endif
+    static constexpr int EPB_OVR = D != 3 ? 0 : (P1 == 5 ? FDG_EPB_P5 : (P1 == 6 ? FDG_EPB_P6 : (P1 == 7 ? FDG_EPB_P7 : 0)));
+    static constexpr int EPB = EPB_OVR > 0 ? EPB_OVR : (LINES >= TT ? 1 : TT / LINES);
     static constexpr int NT = ((EPB * LINES + 31) / 32) * 32;
     static constexpr int FS = EPB * NNP;      // stride of one primitive field
     static constexpr int FA = EPB * NNP + 1;  // stride of one accumulator variable (odd: spreads banks)
@@ -177,13 +191,24 @@ struct Geo {
 // -- 2.7% faster in steady state than 6 CTAs at 168 registers and one wave for
 // cfg2 (profiles/r01_tuning.md); curved kernels spill at 128 registers;
 // others: 6 (p+1 <= 5) or as many as fit.
-template <int D, int P1, int MODE, bool CURVED>
+#ifndef FDG_WARPS_HI
+#define FDG_WARPS_HI 12  // 3D p + 1 = 6, 7: resident warps per SM the register cap aims at (0: no cap).
+#endif                   // 168 registers instead of 254 (N=5 Ranocha VOL 3.35 -> 2.46 ms); p + 1 = 8 holds
+                         // 4 CTAs per SM by shared memory, so a cap would only cost registers
+#ifndef FDG_WARPS_P7_LOG
+#define FDG_WARPS_P7_LOG 8  // p + 1 = 7 with a log-mean flux: 251 registers without spills beat 168 with 384 B
+#endif                      // of them (N=6 Ranocha VOL 3.93 -> 3.34 ms; Shima the other way, 1.91 vs 2.29 ms)
+template <int D, int P1, int MODE, bool CURVED, int VF = -1>
 __host__ __device__ constexpr int min_blocks()
 {
-    // counted in 64-thread CTAs, scaled to the CTA size (same warps per SM)
-    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS
-                              : ((MODE == FAST && D == 3 && P1 <= 4 && !CURVED) ? 8 : (P1 <= 5 ? 6 : 1)) *
-                                    (Geo<D, P1>::NT < 64 ? 64 / Geo<D, P1>::NT : 1);
+    // a target of resident warps per SM (16: 128 registers, 12: 168), turned
+    // into CTAs of this degree's size
+    constexpr bool log_flux = VF == F_RANOCHA || VF == F_CHANDRASHEKAR;
+    constexpr int warps = (MODE == FAST && D == 3 && P1 <= 4 && !CURVED) ? 16
+                          : (P1 <= 5 ? 12
+                             : ((D == 3 && P1 <= 7) ? ((P1 == 7 && log_flux) ? FDG_WARPS_P7_LOG : FDG_WARPS_HI) : 0));
+    constexpr int cta_warps = Geo<D, P1>::NT / 32;
+    return FDG_MIN_BLOCKS > 0 ? FDG_MIN_BLOCKS : (warps / cta_warps > 0 ? warps / cta_warps : 1);
 }
 
 template <int D, int P1, int VF, int LOGS>
@@ -553,6 +578,9 @@ __device__ __forceinline__ int line_stride(int n)  // P1^(D-1-n) without a runti
 #ifndef FDG_RT_DIR_MIN_P1
 #define FDG_RT_DIR_MIN_P1 5  // p+1 = 4: 7% slower; 5: cfg4 RHS +5%; 8: cfg3 +3-16% (profiles/r01_tuning.md)
 #endif
+#ifndef FDG_RT_DIR_MIN_P1_VOLK
+#define FDG_RT_DIR_MIN_P1_VOLK 8  // N=4/5/6 Ranocha VOL: 2.51 -> 2.27, 2.51 -> 2.22, 4.50 -> 3.91 ms
+#endif
 template <int D, int P1, int VF>
 __host__ __device__ constexpr bool runtime_direction()
 {
@@ -613,6 +641,22 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
     const double* w = prm.wts[n];
     constexpr int EH = energy_half(VF) ? 1 : 0;
     [[maybe_unused]] const double* wE = prm.wtsE[n];
+    // curved meshes: the line's metric rows Ja^n (P1 x D values) are loaded
+    // once, all loads in flight together, instead of two rows per pair inside
+    // the pair loop (cfg4 RHS, r02 s5 capture: 13.8% of the stall samples sat
+    // on those loads)
+#ifndef FDG_RT_JL_MAXP1
+#define FDG_RT_JL_MAXP1 5  // with the line's node data in registers too (FDG_RT_LINE_REGS_MAXP1): the pair loop
+                           // runs on registers only, cfg4 RHS 0.925 -> 0.900 ms (either one alone: 0.95 - 0.96 ms)
+#endif
+    constexpr bool JLR = CURVED && P1 <= FDG_RT_JL_MAXP1;
+    [[maybe_unused]] double jl[JLR ? P1 : 1][D];
+    if constexpr (JLR) {
+#pragma unroll
+        for (int a = 0; a < P1; ++a)
+#pragma unroll
+            for (int j = 0; j < D; ++j) jl[a][j] = __ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j);
+    }
     // FDG_FACE_EARLY: where the neighbour-trace loads of the fused interface
     // terms are issued -- 0: after the pair loop (with the fluxes), 1: before
     // the last pair (one flux evaluation hides the L2 latency), 2: before
@@ -625,24 +669,44 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
     if constexpr (EARLY && FDG_FACE_EARLY == 2) {
         if (faces) line_faces_load<D, P1>(prm, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, pf, ml);
     }
+    // whole line in registers up to this degree (P1 shared-memory node loads
+    // per pass instead of P1 + P1 (P1 - 1) / 2)
+#ifndef FDG_RT_LINE_REGS_MAXP1
+#define FDG_RT_LINE_REGS_MAXP1 5  // (with FDG_RT_JL_MAXP1) cfg4 RHS 0.925 -> 0.900 ms, SSPRK43 step 4.38 -> 4.30 ms
+#endif
+    // (not below p + 1 = 5: the p + 1 = 4 RHS twin lives at 128 registers, cfg5 RHS 4.95 -> 5.24 ms with it)
+    constexpr bool LREG = P1 >= 5 && P1 <= FDG_RT_LINE_REGS_MAXP1;
+    [[maybe_unused]] Node<D, NX> qline[LREG ? P1 : 1];
+    if constexpr (LREG) {
+#pragma unroll
+        for (int a = 0; a < P1; ++a) qline[a] = load(a);
+    }
     sfor<0, P1>([&](auto A) {
         constexpr int a = decltype(A)::value;
-        const Node<D, NX> qa = load(a);
+        Node<D, NX> qa;
+        if constexpr (LREG) qa = qline[a];
+        else qa = load(a);
         sfor<a + 1, P1>([&](auto B) {
             constexpr int b = decltype(B)::value;
             if constexpr (EARLY && FDG_FACE_EARLY == 1 && a == P1 - 2 && b == P1 - 1) {
                 if (faces) line_faces_load<D, P1>(prm, vmap, m, base, base + (P1 - 1) * stride, nbm, nbp, pf, ml);
             }
-            const Node<D, NX> qb = load(b);
+            Node<D, NX> qb;
+            if constexpr (LREG) qb = qline[b];
+            else qb = load(b);
             const double wa = w[a * P1 + b];
             const double wb = w[b * P1 + a];
             double f[NVAR];
             if constexpr (CURVED) {
                 double alpha[D];
 #pragma unroll
-                for (int j = 0; j < D; ++j)
-                    alpha[j] = 0.5 * (__ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j) +
-                                      __ldg(prm.ja + ((e * G::NN + base + b * stride) * D + n) * D + j));
+                for (int j = 0; j < D; ++j) {
+                    if constexpr (JLR)
+                        alpha[j] = 0.5 * (jl[a][j] + jl[b][j]);
+                    else
+                        alpha[j] = 0.5 * (__ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j) +
+                                          __ldg(prm.ja + ((e * G::NN + base + b * stride) * D + n) * D + j));
+                }
                 fast_volume_flux<D, VF, -1, LOGS, EH>(qa, qb, alpha, prm.gas.igm1, f, vm);
             } else {
                 fast_volume_flux<D, VF, 0, LOGS, EH>(qa, qb, nullptr, prm.gas.igm1, f, vm);
@@ -814,7 +878,7 @@ extern "C" int fdg_debug_cta_ns(unsigned long long* out, int n)
 // EPIK >= 0 fixes the epilogue at compile time (the volume-integral-only
 // twin: no interface / stage code in the kernel image, fdg_dispatch.cuh)
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC = 0, int EPIK = -1>
-__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE, CURVED>())
+__global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, P1, MODE, CURVED, VF>())
     elem_kernel(const __grid_constant__ KParams prm)
 {
     using G = Geo<D, P1>;
@@ -1090,8 +1154,11 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             // 7.83 -> 6.44 ms with one copy (profiles/r02_tuning.md); the
             // volume-only twin keeps the compile-time passes below p+1 = 5
             // (3.87 vs 4.03 ms: there the rotated-load address math costs more)
+            // (the volume-only twin's small image keeps the compile-time
+            // passes up to p + 1 = 7, FDG_RT_DIR_MIN_P1_VOLK)
             constexpr bool RT_ONLY = MODE == FAST && VF != F_CENTRAL &&
-                                     (runtime_direction<D, P1, VF>() || EPIK == EPI_RHS || EPIK == EPI_STAGE);
+                                     ((EPIK == EPI_VOLUME ? P1 >= FDG_RT_DIR_MIN_P1_VOLK : runtime_direction<D, P1, VF>()) ||
+                                      EPIK == EPI_RHS || EPIK == EPI_STAGE);
             bool rt_pass = RT_ONLY;
             if constexpr (!RT_ONLY && MODE == FAST && runtime_direction_iface<D, P1, VF>())
                 rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;
