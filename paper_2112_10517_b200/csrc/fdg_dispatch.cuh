@@ -45,10 +45,13 @@ constexpr bool has_volk()
 #ifndef FDG_RHSK
 #define FDG_RHSK 1
 #endif
+#ifndef FDG_RHSK_MAXP1
+#define FDG_RHSK_MAXP1 8  // N = 5..7 RHS: 4.50 / 5.17 / 3.81 -> 3.96 / . / 3.42 ms with the twins
+#endif
 template <int D, int P1, int VF, int MODE, bool CURVED>
 constexpr bool has_rhsk()
 {
-    return FDG_RHSK && MODE == FAST && D == 3 && (P1 == 4 || P1 == 5) && VF != F_CENTRAL;
+    return FDG_RHSK && MODE == FAST && D == 3 && P1 >= 4 && P1 <= FDG_RHSK_MAXP1 && VF != F_CENTRAL;
 }
 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int OCC>

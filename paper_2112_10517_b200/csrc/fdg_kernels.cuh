@@ -1156,9 +1156,21 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             // (3.87 vs 4.03 ms: there the rotated-load address math costs more)
             // (the volume-only twin's small image keeps the compile-time
             // passes up to p + 1 = 7, FDG_RT_DIR_MIN_P1_VOLK)
+            // RHS / stage twins: runtime pass at p + 1 = 4 (cfg5 RHS 7.90 -> 6.44 ms when
+            // it went in) and on the curved p + 1 = 5 mesh (cfg4 step 4.30 vs 4.36 ms),
+            // compile-time passes from FDG_RHSK_CT_MINP1 on (Cartesian N = 4 / 5 / 6
+            // Ranocha RHS 3.58 / 3.96 / 4.93 -> 3.31 / 3.14 / 4.17 ms)
+#ifndef FDG_RHSK_CT_MINP1
+#define FDG_RHSK_CT_MINP1 5
+#endif
+#ifndef FDG_RHSK_CT_MAXP1
+#define FDG_RHSK_CT_MAXP1 7
+#endif
+            constexpr bool RHSK_CT = P1 >= FDG_RHSK_CT_MINP1 && P1 <= FDG_RHSK_CT_MAXP1 && !(P1 == 5 && CURVED);
             constexpr bool RT_ONLY = MODE == FAST && VF != F_CENTRAL &&
-                                     ((EPIK == EPI_VOLUME ? P1 >= FDG_RT_DIR_MIN_P1_VOLK : runtime_direction<D, P1, VF>()) ||
-                                      EPIK == EPI_RHS || EPIK == EPI_STAGE);
+                                     (EPIK == EPI_VOLUME ? P1 >= FDG_RT_DIR_MIN_P1_VOLK
+                                      : (EPIK == EPI_RHS || EPIK == EPI_STAGE) ? !RHSK_CT
+                                                                               : runtime_direction<D, P1, VF>());
             bool rt_pass = RT_ONLY;
             if constexpr (!RT_ONLY && MODE == FAST && runtime_direction_iface<D, P1, VF>())
                 rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;

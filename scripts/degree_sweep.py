@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--degrees", default="3,4,5,6,7")
     ap.add_argument("--fluxes", default="ranocha,shima")
+    ap.add_argument("--what", default="volume", choices=["volume", "rhs"],
+                    help="rhs: the full RHS (Rusanov interfaces), fractions against the volume integral's bound")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     hbm, peak_src = bench._peaks()
@@ -53,13 +55,14 @@ def main():
             dm = device_mesh_for(setup)
             scheme = config.scheme()
             out = dm.empty()
+            launch = dm.rhs if args.what == "rhs" else dm.volume
             for _ in range(args.warmup):
-                dm.volume(u, scheme, out=out)
+                launch(u, scheme, out=out)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(args.steps):
-                dm.volume(u, scheme, out=out)
+                launch(u, scheme, out=out)
             b.record(stream)
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / args.steps
@@ -69,7 +72,7 @@ def main():
             hbm_frac = 80.0 * rate / 1e9 / hbm
             fp_frac = flop * rate / 1e12 / fp64_peak
             print(json.dumps({
-                "N": p, "dims": DIMS[p], "flux": flux, "precompute": config.precompute, "nodes": nodes,
+                "what": args.what, "N": p, "dims": DIMS[p], "flux": flux, "precompute": config.precompute, "nodes": nodes,
                 "state_mb": u.numel() * 8 / 1e6, "ms": ms, "nodes_per_s": rate,
                 "flop_per_node": flop, "hbm_frac": hbm_frac, "fp64_frac": fp_frac,
                 "bound": "fp64" if fp_frac > hbm_frac else "hbm", "roofline_frac": max(hbm_frac, fp_frac),
