@@ -464,7 +464,7 @@ __device__ __forceinline__ void line_faces(const KParams& prm, long long e, int 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST = (N == 0)>
 __device__ __forceinline__ void volume_direction(const KParams& prm, const double* sq, double* sacc, int el,
                                                  int m, long long e, unsigned vm, bool faces = false, int nbm = 0,
-                                                 int nbp = 0)
+                                                 int nbp = 0, double* aos = nullptr)
 {
     using G = Geo<D, P1>;
     constexpr int NVAR = G::NVAR;
@@ -550,6 +550,22 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
                                                         acc[P1 - 1], sq, sbase + G::pad(nodes[0]),
                                                         sbase + G::pad(nodes[P1 - 1]));
         }
+    }
+    // FDG_AOS_LAST: the last pass of a volume-only launch (lines of P1
+    // consecutive nodes; values final: 1/J is folded into the weights) leaves
+    // its results as AoS straight in the primitive region for the bulk store
+    // -- once every thread of the CTA is past its pair loop, nothing reads the
+    // primitives any more -- instead of SoA accumulators that the epilogue
+    // reads back and transposes (40 shared-memory instructions per thread).
+    // Called by every thread of the CTA (the barrier).
+    if (aos) {
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < P1; ++a)
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) aos[(el * G::NN + nodes[a]) * NVAR + v] = acc[a][v];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        return;
     }
 #pragma unroll
     for (int a = 0; a < P1; ++a)
@@ -742,14 +758,15 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
 
 template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST>
 __device__ __forceinline__ void vdir(const KParams& prm, const double* sq, double* sacc, int el, int m, long long e,
-                                     bool active, unsigned vm, bool fuse = false, const int* nb = nullptr)
+                                     bool active, unsigned vm, bool fuse = false, const int* nb = nullptr,
+                                     double* aos = nullptr)
 {
     if constexpr (MODE == FAST) {
         if (vm) {
             const bool faces = fuse && active;
             volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, active ? e : e - el, vm,
                                                                        faces, faces ? nb[(el * D + N) * 2] : 0,
-                                                                       faces ? nb[(el * D + N) * 2 + 1] : 0);
+                                                                       faces ? nb[(el * D + N) * 2 + 1] : 0, aos);
         }
     } else {
         if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, e, 0u);
@@ -1174,6 +1191,17 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
             bool rt_pass = RT_ONLY;
             if constexpr (!RT_ONLY && MODE == FAST && runtime_direction_iface<D, P1, VF>())
                 rt_pass = (epi != EPI_VOLUME) && prm.rt_iface;
+#ifndef FDG_AOS_LAST
+#define FDG_AOS_LAST 1
+#endif
+            // results straight to the bulk-store staging from the last compile-time
+            // pass (lines of consecutive nodes): the volume-only twin on Cartesian
+            // meshes whose CTAs have no idle threads (the barrier inside). In the
+            // runtime-direction pass the same measured slower (cfg5 RHS 4.95 ->
+            // 5.50 ms, cfg3 VOL 0.877 -> 0.982 ms), so only here.
+            constexpr bool AOS_OK = FDG_AOS_LAST && EPIK == EPI_VOLUME && MODE == FAST && !CURVED && !REV && D == 3 &&
+                                    USED == NT;
+            const bool aos_on = AOS_OK && prm.jac_folded && tma_out;
             if (rt_pass) {
                 if constexpr (MODE == FAST && VF != F_CENTRAL) {
 #pragma unroll 1
@@ -1196,8 +1224,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                 __syncthreads();
                 FDG_PT(3)
                 if constexpr (D == 3) {
-                    vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? 0 : 2, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
+                    double* aos = aos_on ? sq : nullptr;
+                    vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? 0 : 2, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb,
+                                                                            aos);
                     __syncthreads();
+                    if (aos) {
+                        if (tid == 0) bulk_store(prm.out + base, sq, (unsigned)count * 8u);
+                        tma_pending = true;
+                        continue;
+                    }
                 }
             }
             FDG_PT(4)
