@@ -478,11 +478,11 @@ struct Gas {
 };
 
 // Volume two-point flux dispatch (compile-time kind).
-template <int D, int VF, int AXIS, int MODE, int LOGS, int EH = 0, int NX>
+template <int D, int VF, int AXIS, int MODE, int LOGS, int EH = 0, int KP = 0, int NX>
 __device__ __forceinline__ void volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                             const Gas& gas, int pre, double* f, unsigned vm)
 {
-    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS, EH>(l, r, nrm, gas.igm1, f, vm);
+    if constexpr (MODE == FAST) fast_volume_flux<D, VF, AXIS, LOGS, EH, KP>(l, r, nrm, gas.igm1, f, vm);
     else if constexpr (VF == F_SHIMA) flux_shima<D, AXIS, MODE>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_RANOCHA) flux_ranocha<D, AXIS, MODE, LOGS>(l, r, nrm, gas.igm1, f);
     else if constexpr (VF == F_CENTRAL) flux_central<D, AXIS, MODE>(l, r, nrm, gas.igm1, pre != PRE_NONE, f);

@@ -388,7 +388,9 @@ __device__ __forceinline__ void fast_kg(const Node<D, NX>& l, const Node<D, NX>&
 }
 
 // Chandrashekar; x[0] = beta = rho/(2p), x[1] = log rho, x[2] = log beta (LOGS)
-template <int D, int AXIS, int LOGS, int NX>
+// KP: the node's pressure slot holds |v/2|^2 instead (volume-only launches:
+// this flux never reads p, and {|v|^2}/2 becomes one add instead of 2 d FMAs)
+template <int D, int AXIS, int LOGS, int KP = 0, int NX>
 __device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                                    double igm1, double* f, unsigned vm)
 {
@@ -410,8 +412,12 @@ __device__ __forceinline__ void fast_chandrashekar(const Node<D, NX>& l, const N
     const double vn_avg = hdot<D, AXIS>(l.v, nrm) + hdot<D, AXIS>(r.v, nrm);
     const double f_rho = rho_mean * vn_avg;
     double v2 = 0.0;  // {|v|^2}/2 = |vh_l|^2 + |vh_r|^2
+    if constexpr (KP) {
+        v2 = l.p + r.p;
+    } else {
 #pragma unroll
-    for (int i = 0; i < D; ++i) v2 = fma(l.v[i], l.v[i], fma(r.v[i], r.v[i], v2));
+        for (int i = 0; i < D; ++i) v2 = fma(l.v[i], l.v[i], fma(r.v[i], r.v[i], v2));
+    }
     f[0] = f_rho;
     double work = 0.0;
 #pragma unroll
@@ -510,7 +516,7 @@ __device__ __forceinline__ Node<D, n_extra(VF, LOGS)> make_node_fast(const doubl
 // volume kinds whose FAST energy flux can come back halved (EH = 1)
 __host__ __device__ constexpr bool energy_half(int vf) { return vf == F_RANOCHA; }
 
-template <int D, int VF, int AXIS, int LOGS, int EH = 0, int NX>
+template <int D, int VF, int AXIS, int LOGS, int EH = 0, int KP = 0, int NX>
 __device__ __forceinline__ void fast_volume_flux(const Node<D, NX>& l, const Node<D, NX>& r, const double* nrm,
                                                  double igm1, double* f, unsigned vm)
 {
@@ -518,7 +524,7 @@ __device__ __forceinline__ void fast_volume_flux(const Node<D, NX>& l, const Nod
     else if constexpr (VF == F_RANOCHA) fast_ranocha<D, AXIS, LOGS, EH>(l, r, nrm, igm1, f, vm);
     else if constexpr (VF == F_CENTRAL) fast_central<D, AXIS>(l, r, nrm, f);
     else if constexpr (VF == F_KG) fast_kg<D, AXIS>(l, r, nrm, f);
-    else fast_chandrashekar<D, AXIS, LOGS>(l, r, nrm, igm1, f, vm);
+    else fast_chandrashekar<D, AXIS, LOGS, KP>(l, r, nrm, igm1, f, vm);
 }
 
 }  // namespace fdg

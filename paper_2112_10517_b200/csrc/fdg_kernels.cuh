@@ -92,6 +92,9 @@ struct KParams {
 #ifndef FDG_MIN_BLOCKS
 #define FDG_MIN_BLOCKS 0  // 0: per-degree default below
 #endif
+#ifndef FDG_CHANDRA_KP
+#define FDG_CHANDRA_KP 1  // volume-only Chandrashekar twins: |v/2|^2 staged in the unused pressure slot
+#endif
 #ifndef FDG_LINE_REGS
 #define FDG_LINE_REGS 1  // compile-time passes: the line's node data in registers (r02: cfg5 VOL 3.52 -> 3.49 ms)
 #endif
@@ -461,7 +464,13 @@ __device__ __forceinline__ void line_faces(const KParams& prm, long long e, int 
 }
 
 // One direction of the volume integral for the thread's line.
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST = (N == 0)>
+// KP: FAST Chandrashekar nodes of a volume-only launch carry |v/2|^2 in the pressure slot
+template <int D, int P1, int VF, int MODE, int EPIK>
+__host__ __device__ constexpr int kin_in_p()
+{
+    return (FDG_CHANDRA_KP && MODE == FAST && VF == F_CHANDRASHEKAR && EPIK == 0 /* EPI_VOLUME */) ? 1 : 0;
+}
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST = (N == 0), int KP = 0>
 __device__ __forceinline__ void volume_direction(const KParams& prm, const double* sq, double* sacc, int el,
                                                  int m, long long e, unsigned vm, bool faces = false, int nbm = 0,
                                                  int nbp = 0, double* aos = nullptr)
@@ -526,9 +535,9 @@ __device__ __forceinline__ void volume_direction(const KParams& prm, const doubl
                 double alpha[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) alpha[j] = 0.5 * (jl[a][j] + jl[b][j]);
-                volume_flux<D, VF, -1, MODE, LOGS, EH>(qa, qb, alpha, prm.gas, prm.precompute, f, vm);
+                volume_flux<D, VF, -1, MODE, LOGS, EH, KP>(qa, qb, alpha, prm.gas, prm.precompute, f, vm);
             } else {
-                volume_flux<D, VF, N, MODE, LOGS, EH>(qa, qb, nullptr, prm.gas, prm.precompute, f, vm);
+                volume_flux<D, VF, N, MODE, LOGS, EH, KP>(qa, qb, nullptr, prm.gas, prm.precompute, f, vm);
             }
 #pragma unroll
             for (int v = 0; v < NVAR - EH; ++v) {
@@ -616,7 +625,7 @@ __host__ __device__ constexpr bool runtime_direction_iface()
     return FDG_RT_DIR_IFACE && VF != F_CENTRAL && !runtime_direction<D, P1, VF>();
 }
 
-template <int D, int P1, int VF, bool CURVED, int LOGS>
+template <int D, int P1, int VF, bool CURVED, int LOGS, int KP = 0>
 __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const double* sq, double* sacc, int el, int m,
                                                     long long e, int n, bool first, unsigned vm, bool faces = false,
                                                     int nbm = 0, int nbp = 0)
@@ -723,9 +732,9 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
                         alpha[j] = 0.5 * (__ldg(prm.ja + ((e * G::NN + base + a * stride) * D + n) * D + j) +
                                           __ldg(prm.ja + ((e * G::NN + base + b * stride) * D + n) * D + j));
                 }
-                fast_volume_flux<D, VF, -1, LOGS, EH>(qa, qb, alpha, prm.gas.igm1, f, vm);
+                fast_volume_flux<D, VF, -1, LOGS, EH, KP>(qa, qb, alpha, prm.gas.igm1, f, vm);
             } else {
-                fast_volume_flux<D, VF, 0, LOGS, EH>(qa, qb, nullptr, prm.gas.igm1, f, vm);
+                fast_volume_flux<D, VF, 0, LOGS, EH, KP>(qa, qb, nullptr, prm.gas.igm1, f, vm);
             }
 #pragma unroll
             for (int v = 0; v < NVAR - EH; ++v) {
@@ -756,7 +765,7 @@ __device__ __forceinline__ void volume_direction_rt(const KParams& prm, const do
     }
 }
 
-template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST>
+template <int D, int P1, int VF, bool CURVED, int MODE, int LOGS, int N, bool FIRST, int KP = 0>
 __device__ __forceinline__ void vdir(const KParams& prm, const double* sq, double* sacc, int el, int m, long long e,
                                      bool active, unsigned vm, bool fuse = false, const int* nb = nullptr,
                                      double* aos = nullptr)
@@ -764,12 +773,12 @@ __device__ __forceinline__ void vdir(const KParams& prm, const double* sq, doubl
     if constexpr (MODE == FAST) {
         if (vm) {
             const bool faces = fuse && active;
-            volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, active ? e : e - el, vm,
+            volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST, KP>(prm, sq, sacc, el, m, active ? e : e - el, vm,
                                                                        faces, faces ? nb[(el * D + N) * 2] : 0,
                                                                        faces ? nb[(el * D + N) * 2 + 1] : 0, aos);
         }
     } else {
-        if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST>(prm, sq, sacc, el, m, e, 0u);
+        if (active) volume_direction<D, P1, VF, CURVED, MODE, LOGS, N, FIRST, KP>(prm, sq, sacc, el, m, e, 0u);
     }
 }
 
@@ -901,6 +910,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
     using G = Geo<D, P1>;
     constexpr int NN = G::NN, NVAR = G::NVAR, EPB = G::EPB, NT = G::NT;
     constexpr int NX = n_extra(VF, LOGS);
+    constexpr int KP = kin_in_p<D, P1, VF, MODE, EPIK>();
     constexpr int KU = (EPB * NN * NVAR + NT - 1) / NT;  // state values per thread
     constexpr int KN = (EPB * NN + NT - 1) / NT;         // nodes per thread
     extern __shared__ double smem[];
@@ -1140,13 +1150,19 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                     if (t < ne * NN) {
                         const int tel = t / NN, node = t - tel * NN;
                         const double* su = sacc + t * NVAR;
-                        const Node<D, NX> q = make_node<D, VF, MODE, LOGS, EPIK == EPI_VOLUME>(su, prm.gas.gm1);
+                        Node<D, NX> q = make_node<D, VF, MODE, LOGS, EPIK == EPI_VOLUME>(su, prm.gas.gm1);
                         if constexpr (MODE == FAST) {
                             const int g = gate_fast<D>(su, q.p, prm.gas.gm1);  // 1 ok, 0 bad, -1 undecided
                             slow |= (g < 0) ? (1u << k) : 0u;
                             bad = (g == 0 && (unsigned)t < bad) ? (unsigned)t : bad;
                         } else {
                             bad = (!gate_ok<D>(su, prm.gas.gm1) && (unsigned)t < bad) ? (unsigned)t : bad;
+                        }
+                        if constexpr (KP) {  // (after the gate, which reads the half pressure)
+                            double s2 = 0.0;
+#pragma unroll
+                            for (int i = 0; i < D; ++i) s2 = fma(q.v[i], q.v[i], s2);
+                            q.p = s2;
                         }
                         store_node<D, NX>(sq, G::FS, tel * G::NNP + G::pad(node), q);
                     }
@@ -1209,7 +1225,7 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                         const int n = REV ? D - 1 - i : i;
                         if (vmask) {
                             const bool faces = fuse && active;
-                            volume_direction_rt<D, P1, VF, CURVED, LOGS>(prm, sq, sacc, el, m, active ? e : e - el, n, i == 0,
+                            volume_direction_rt<D, P1, VF, CURVED, LOGS, KP>(prm, sq, sacc, el, m, active ? e : e - el, n, i == 0,
                                                                          vmask, faces, faces ? s_nb[(el * D + n) * 2] : 0,
                                                                          faces ? s_nb[(el * D + n) * 2 + 1] : 0);
                         }
@@ -1217,15 +1233,15 @@ __global__ void __launch_bounds__(Geo<D, P1>::NT, OCC > 0 ? OCC : min_blocks<D, 
                     }
                 }
             } else if constexpr (!RT_ONLY) {
-                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 1 : 0, true>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
+                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 1 : 0, true, KP>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
                 __syncthreads();
                 FDG_PT(2)
-                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 2 : 1, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
+                vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? D - 2 : 1, false, KP>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb);
                 __syncthreads();
                 FDG_PT(3)
                 if constexpr (D == 3) {
                     double* aos = aos_on ? sq : nullptr;
-                    vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? 0 : 2, false>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb,
+                    vdir<D, P1, VF, CURVED, MODE, LOGS, REV ? 0 : 2, false, KP>(prm, sq, sacc, el, m, e, active, vmask, fuse, s_nb,
                                                                             aos);
                     __syncthreads();
                     if (aos) {
